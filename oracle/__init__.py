@@ -1,0 +1,313 @@
+"""ctypes shim over oracle/oracle.c — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+leg may import this module. It never touches the CUDA library and the CUDA
+library never touches it.
+
+Paper citations for every routine are in oracle/oracle.c's header and at each
+function there (PAPER.md line numbers, SURVEY.md §8(c) readings).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-std=c11", "-fPIC", "-shared",
+          "-D_POSIX_C_SOURCE=199309L"]
+_lock = threading.Lock()
+_lib = None
+
+MODE_FULL, MODE_PRIMAL_ONLY, MODE_NONE = 0, 1, 2
+STATUS = {0: "converged", 1: "iter_limit", 2: "time_limit", 3: "numerical_failure", -1: "running"}
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain C, no SIMD/OpenMP, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class LPStruct(C.Structure):
+    _fields_ = [("m", C.c_int32), ("n", C.c_int32),
+                ("Ap", C.c_void_p), ("Aj", C.c_void_p), ("Ax", C.c_void_p),
+                ("ATp", C.c_void_p), ("ATj", C.c_void_p), ("ATx", C.c_void_p),
+                ("b", C.c_void_p)]
+
+
+class Params(C.Structure):
+    _fields_ = [("eps_rel", C.c_double), ("eps_abs", C.c_double), ("max_iters", C.c_int64),
+                ("time_limit_s", C.c_double), ("check_every", C.c_int32),
+                ("step_scale", C.c_double), ("step_size", C.c_double),
+                ("power_iters", C.c_int32), ("seed", C.c_uint64),
+                ("primal_weight", C.c_double), ("restart", C.c_int32),
+                ("beta_suff", C.c_double), ("beta_nec", C.c_double),
+                ("beta_art", C.c_double), ("theta", C.c_double)]
+
+
+class Result(C.Structure):
+    _fields_ = [("status", C.c_int32), ("returned_average", C.c_int32),
+                ("iterations", C.c_int64), ("restarts", C.c_int64),
+                ("pobj", C.c_double), ("dobj", C.c_double), ("gap", C.c_double),
+                ("rp_norm", C.c_double), ("rd_norm", C.c_double), ("score", C.c_double),
+                ("step_size", C.c_double), ("primal_weight", C.c_double), ("wall_s", C.c_double)]
+
+
+class Score(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("rp", "rd", "pobj", "dobj", "r_p", "r_d", "r_g", "score")]
+
+
+class Stats(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("off_bound", "off_bound_strict", "off_bound_model",
+                                         "zero_rc", "candidates", "fix_lb", "fix_ub",
+                                         "est_primal_pushes", "est_dual_pushes")] + \
+               [("is_candidate", C.c_int32)]
+
+
+def _as_dict(s):
+    return {k: getattr(s, k) for k, _ in s._fields_}
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = C.CDLL(build())
+            P = C.c_void_p
+            L.orc_splitmix.restype = C.c_uint64
+            L.orc_splitmix.argtypes = [C.c_uint64, C.c_int64]
+            L.orc_u01.restype = C.c_double
+            L.orc_u01.argtypes = [C.c_uint64, C.c_int64]
+            L.orc_transpose.argtypes = [C.c_int32, C.c_int32, P, P, P, P, P, P]
+            L.orc_spmv.argtypes = [C.c_int32, P, P, P, P, P]
+            L.orc_norm2.restype = C.c_double
+            L.orc_norm2.argtypes = [C.c_int64, P]
+            L.orc_score.argtypes = [C.POINTER(LPStruct), P, P, P, C.c_double, C.c_double, P, P,
+                                    C.POINTER(Score)]
+            L.orc_power_sigma.restype = C.c_double
+            L.orc_power_sigma.argtypes = [C.POINTER(LPStruct), C.c_int32, C.c_uint64]
+            L.orc_create.restype = P
+            L.orc_create.argtypes = [C.POINTER(LPStruct), C.POINTER(Params), P, P, P, P, P,
+                                     C.c_int, C.c_double, C.c_int64, C.c_double]
+            L.orc_run.restype = C.c_int
+            L.orc_run.argtypes = [P, C.c_int64]
+            L.orc_get.argtypes = [P, P, P]
+            L.orc_result_of.argtypes = [P, C.POINTER(Result)]
+            L.orc_destroy.argtypes = [P]
+            L.orc_get_eta.restype = C.c_double
+            L.orc_get_eta.argtypes = [P]
+            L.orc_get_omega.restype = C.c_double
+            L.orc_get_omega.argtypes = [P]
+            L.orc_get_k.restype = C.c_int64
+            L.orc_get_k.argtypes = [P]
+            L.orc_reduced_costs.argtypes = [C.POINTER(LPStruct), P, P, P]
+            L.orc_corner_model.argtypes = [C.c_int32, P, P, P, P, C.c_double, C.c_double,
+                                           C.c_uint64, P, P, P, C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_int64)]
+            L.orc_stats.argtypes = [C.c_int32, C.c_int32, P, P, P, P, P, P, C.c_double,
+                                    C.c_int64, C.POINTER(Stats)]
+            _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _f64(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+def default_params(**kw) -> Params:
+    """Defaults of SURVEY §8(b) cpd_params (same meaning as the CUDA side's)."""
+    p = Params(eps_rel=1e-4, eps_abs=1e-6, max_iters=100000, time_limit_s=0.0, check_every=64,
+               step_scale=0.9, step_size=0.0, power_iters=128, seed=7, primal_weight=0.0,
+               restart=1, beta_suff=0.2, beta_nec=0.8, beta_art=0.36, theta=0.5)
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+class OracleLP:
+    """The oracle's own copy of an LP: CSR(A^T) from the generator, CSR(A) built
+    by the oracle's counting-sort transpose (orc_transpose)."""
+
+    def __init__(self, lp):
+        L = lib()
+        self.m, self.n = int(lp.m), int(lp.n)
+        self.ATp = np.ascontiguousarray(lp.ATp, dtype=np.int32)
+        self.ATj = np.ascontiguousarray(lp.ATj, dtype=np.int32)
+        self.ATx = _f64(lp.ATx)
+        nnz = int(self.ATp[-1])
+        self.Ap = np.zeros(self.m + 1, dtype=np.int32)
+        self.Aj = np.zeros(max(nnz, 1), dtype=np.int32)
+        self.Ax = np.zeros(max(nnz, 1), dtype=np.float64)
+        L.orc_transpose(self.n, self.m, _p(self.ATp), _p(self.ATj), _p(self.ATx),
+                        _p(self.Ap), _p(self.Aj), _p(self.Ax))
+        self.b = _f64(lp.b)
+        self.c = _f64(lp.c)
+        self.lb = _f64(lp.lb)
+        self.ub = _f64(lp.ub)
+        self.s = LPStruct(self.m, self.n, _p(self.Ap), _p(self.Aj), _p(self.Ax),
+                          _p(self.ATp), _p(self.ATj), _p(self.ATx), _p(self.b))
+        self.nb = float(L.orc_norm2(self.m, _p(self.b)))
+
+    def A_times(self, v):
+        out = np.zeros(self.m)
+        v = _f64(v)
+        lib().orc_spmv(self.m, _p(self.Ap), _p(self.Aj), _p(self.Ax), _p(v), _p(out))
+        return out
+
+    def AT_times(self, v):
+        out = np.zeros(self.n)
+        v = _f64(v)
+        lib().orc_spmv(self.n, _p(self.ATp), _p(self.ATj), _p(self.ATx), _p(v), _p(out))
+        return out
+
+
+def score(olp: OracleLP, x, y, c=None, lb=None, ub=None):
+    c = olp.c if c is None else _f64(c)
+    lb = olp.lb if lb is None else _f64(lb)
+    ub = olp.ub if ub is None else _f64(ub)
+    L = lib()
+    nc = float(L.orc_norm2(olp.n, _p(c)))
+    out = Score()
+    x = _f64(x)
+    y = _f64(y)
+    L.orc_score(C.byref(olp.s), _p(c), _p(lb), _p(ub), olp.nb, nc, _p(x), _p(y), C.byref(out))
+    return _as_dict(out)
+
+
+def power_sigma(olp: OracleLP, iters=128, seed=7) -> float:
+    return float(lib().orc_power_sigma(C.byref(olp.s), iters, seed))
+
+
+def u01(seed, j) -> float:
+    return float(lib().orc_u01(seed, j))
+
+
+def splitmix(seed, j) -> int:
+    return int(lib().orc_splitmix(seed, j))
+
+
+class Run:
+    """One R-PDHG run; supports lockstep stepping for parity."""
+
+    def __init__(self, olp: OracleLP, params: Params, c=None, lb=None, ub=None, x_init=None,
+                 y_init=None, mode=MODE_FULL, target=0.0, min_iters=0, eta=0.0):
+        self.olp = olp
+        self.params = params
+        self._keep = [_f64(c) if c is not None else olp.c, _f64(lb) if lb is not None else olp.lb,
+                      _f64(ub) if ub is not None else olp.ub, _f64(x_init), _f64(y_init)]
+        cc, ll, uu, xi, yi = self._keep
+        self.h = lib().orc_create(C.byref(olp.s), C.byref(params), _p(cc), _p(ll), _p(uu),
+                                  _p(xi), _p(yi), mode, target, min_iters, eta)
+
+    def run(self, steps) -> int:
+        return int(lib().orc_run(self.h, steps))
+
+    @property
+    def k(self):
+        return int(lib().orc_get_k(self.h))
+
+    @property
+    def eta(self):
+        return float(lib().orc_get_eta(self.h))
+
+    @property
+    def omega(self):
+        return float(lib().orc_get_omega(self.h))
+
+    def get(self):
+        x = np.zeros(self.olp.n)
+        y = np.zeros(self.olp.m)
+        lib().orc_get(self.h, _p(x), _p(y))
+        return x, y
+
+    def result(self) -> dict:
+        r = Result()
+        lib().orc_result_of(self.h, C.byref(r))
+        return _as_dict(r)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            lib().orc_destroy(h)
+            self.h = None
+
+
+def solve(olp: OracleLP, params: Params = None, **kw):
+    """Phase 1: R-PDHG to eps_rel (or the limits). Returns (x, y, result)."""
+    params = params or default_params()
+    r = Run(olp, params, **kw)
+    r.run(np.iinfo(np.int64).max)
+    x, y = r.get()
+    return x, y, r.result()
+
+
+def reduced_costs(olp: OracleLP, y, c=None):
+    z = np.zeros(olp.n)
+    c = olp.c if c is None else _f64(c)
+    y = _f64(y)
+    lib().orc_reduced_costs(C.byref(olp.s), _p(c), _p(y), _p(z))
+    return z
+
+
+def corner_model(olp: OracleLP, x, z, eps_abs=1e-6, obj_scale=1.0, seed=1001, lb=None, ub=None):
+    """Algorithm 1 line 2: (lhat, uhat, chat, fix_lb, fix_ub)."""
+    n = olp.n
+    lh, uh, ch = np.zeros(n), np.zeros(n), np.zeros(n)
+    fl, fu = C.c_int64(0), C.c_int64(0)
+    # keep every converted array alive across the call (pointers are borrowed)
+    x, z = _f64(x), _f64(z)
+    lb = olp.lb if lb is None else _f64(lb)
+    ub = olp.ub if ub is None else _f64(ub)
+    lib().orc_corner_model(n, _p(x), _p(z), _p(lb), _p(ub),
+                           eps_abs, obj_scale, seed, _p(lh), _p(uh), _p(ch),
+                           C.byref(fl), C.byref(fu))
+    return lh, uh, ch, int(fl.value), int(fu.value)
+
+
+def stats(m, x, z=None, lb=None, ub=None, lhat=None, uhat=None, eps_abs=1e-6, floor=100_000):
+    """Corner statistics a10."""
+    x = _f64(x)
+    n = x.size
+    out = Stats()
+    z, lb, ub, lhat, uhat = (_f64(a) for a in (z, lb, ub, lhat, uhat))
+    lib().orc_stats(m, n, _p(x), _p(z), _p(lb), _p(ub), _p(lhat), _p(uhat), eps_abs, floor,
+                    C.byref(out))
+    return _as_dict(out)
+
+
+def corner_push(olp: OracleLP, x, y, params: Params = None, eps_abs=1e-6, obj_scale=1.0,
+                seed=1001, obj=None, min_iters=100, max_iters=100000, eta=0.0, floor=100_000):
+    """Algorithm 1 with the P:391-395 stop: returns (xhat, y, z, result,
+    stats_before, stats_after, model). y, z are phase-1's."""
+    params = params or default_params()
+    z = reduced_costs(olp, y)
+    lh, uh, ch, fl, fu = corner_model(olp, x, z, eps_abs, obj_scale, seed)
+    if obj is not None:
+        ch = _f64(obj)
+    before = stats(olp.m, x, z, olp.lb, olp.ub, lh, uh, eps_abs, floor)
+    p2 = default_params(**{k: getattr(params, k) for k, _ in Params._fields_})
+    p2.max_iters = max_iters
+    p2.primal_weight = 0.0   # fresh omega from ||chat||/||b|| (S-8)
+    target = params.eps_rel * (1.0 + olp.nb)
+    r = Run(olp, p2, c=ch, lb=lh, ub=uh, x_init=x, y_init=None, mode=MODE_PRIMAL_ONLY,
+            target=target, min_iters=min_iters, eta=eta)
+    r.run(np.iinfo(np.int64).max)
+    xh, _ = r.get()
+    res = r.result()
+    after = stats(olp.m, xh, z, olp.lb, olp.ub, lh, uh, eps_abs, floor)
+    before["fix_lb"] = after["fix_lb"] = fl
+    before["fix_ub"] = after["fix_ub"] = fu
+    return xh, y, z, res, before, after, dict(lhat=lh, uhat=uh, chat=ch, target=target)

@@ -1,0 +1,470 @@
+/*
+ * ORACLE — plain, slow, single-threaded fp64 CPU implementation of the hot path
+ * of "Corner push PDHG" (arXiv 2511.13894).  TEST INFRASTRUCTURE ONLY: only
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * leg may load or call it.  It shares no code with the CUDA path
+ * (paper_2511_13894_b200/csrc) and neither includes the other.
+ *
+ * Compiled: gcc -O2 -fno-fast-math -ffp-contract=off -shared -fPIC (no SIMD
+ * intrinsics, no OpenMP, no BLAS).  Every formula below is written as the paper
+ * (or the SURVEY.md §8(c) reading of it, listed in DESIGN.md "Readings") states
+ * it, with no blocking, fusion or algebraic rewriting:
+ *
+ *   P:64-87    primal/dual pair  min c^T x, Ax=b, x>=0 | max b^T y, A^T y + z = c, z>=0
+ *   P:89-92    general bounds handled implicitly -> projection onto [l,u] (S-6, S-14)
+ *   P:109-117  r_P = b - A x,  r_D = c - A^T y - z
+ *   P:119-131  relative termination tests (2-norms), converged <=> all three hold
+ *   P:21-27, P:412-414 + SURVEY §8(c) R-PDHG   the iteration (S-1..S-5, S-16)
+ *   P:268-293  Algorithm 1 (corner model M^: bound map, Uniform[0,1]^n objective,
+ *              warm start (x, 0)), P:318-329 + P:391-395 early termination
+ *   P:200-210, P:330-381, P:438-452   off-bound / zero-reduced-cost counts,
+ *              push estimates, candidate criterion
+ *
+ * Pins (tests/test_oracle_*.py, `-m "not gpu"`): 2x2 hand-stepped iterate
+ * (tests/golden/pdhg_2x2.json), 1x1 closed form, dense recomputation of
+ * residuals, certificate fixed point, SVD / closed-form operator norms, brute
+ * force vertex enumeration + HiGHS optima, SplitMix64 published outputs,
+ * Algorithm-1 bound-map and count examples.  Iteration COUNTS to eps have no
+ * closed form: "parity unpinned" beyond this file.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+/* ------------------------------------------------------------------ types */
+typedef struct {
+    int32_t m, n;
+    const int32_t *Ap, *Aj; const double *Ax;     /* CSR(A)   (m rows) */
+    const int32_t *ATp, *ATj; const double *ATx;  /* CSR(A^T) (n rows) */
+    const double *b;                              /* m */
+} orc_lp;
+
+typedef struct {
+    double eps_rel, eps_abs;
+    int64_t max_iters;
+    double time_limit_s;
+    int32_t check_every;     /* K: restart-check cadence on t (PDLP lineage) */
+    double step_scale;       /* eta = step_scale / sigma_hat */
+    double step_size;        /* > 0: eta given explicitly */
+    int32_t power_iters;     /* K_pow */
+    uint64_t seed;           /* power-iteration start vector seed */
+    double primal_weight;    /* > 0: omega0 given explicitly */
+    int32_t restart;         /* 0 none, 1 adaptive restart to average/current */
+    double beta_suff, beta_nec, beta_art, theta;
+} orc_params;
+
+typedef struct {
+    int32_t status;          /* 0 converged, 1 iter limit, 2 time limit, 3 numerical failure, -1 running */
+    int32_t returned_average;
+    int64_t iterations, restarts;
+    double pobj, dobj, gap, rp_norm, rd_norm, score, step_size, primal_weight, wall_s;
+} orc_result;
+
+typedef struct {
+    double rp, rd, pobj, dobj, r_p, r_d, r_g, score;
+} orc_score_t;
+
+typedef struct {
+    int64_t off_bound, off_bound_strict, off_bound_model, zero_rc, candidates,
+            fix_lb, fix_ub, est_primal_pushes, est_dual_pushes;
+    int32_t is_candidate;
+} orc_stats_t;
+
+enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2 };
+
+/* ---------------------------------------------------------- basic helpers */
+
+/* Counter-based U[0,1): SplitMix64 finalizer of seed + (j+1)*golden (SURVEY §8(c)
+ * "U(seed, j)"); the (j+1)-th output of a SplitMix64 stream seeded with `seed`. */
+uint64_t orc_splitmix(uint64_t seed, int64_t j)
+{
+    uint64_t s = seed + (uint64_t)(j + 1) * 0x9E3779B97F4A7C15ULL;
+    s = (s ^ (s >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    s = (s ^ (s >> 27)) * 0x94D049BB133111EBULL;
+    s ^= s >> 31;
+    return s;
+}
+
+double orc_u01(uint64_t seed, int64_t j)
+{
+    return (double)(orc_splitmix(seed, j) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+/* CSR transpose by counting sort (the oracle's own loader). */
+void orc_transpose(int32_t nrows, int32_t ncols, const int32_t *p, const int32_t *j,
+                   const double *x, int32_t *tp, int32_t *tj, double *tx)
+{
+    int64_t *next = (int64_t *)calloc((size_t)ncols + 1, sizeof(int64_t));
+    for (int32_t r = 0; r < nrows; ++r)
+        for (int64_t k = p[r]; k < p[r + 1]; ++k) next[j[k] + 1]++;
+    for (int32_t c = 0; c < ncols; ++c) next[c + 1] += next[c];
+    for (int32_t c = 0; c <= ncols; ++c) tp[c] = (int32_t)next[c];
+    for (int32_t r = 0; r < nrows; ++r)
+        for (int64_t k = p[r]; k < p[r + 1]; ++k) {
+            int64_t d = next[j[k]]++;
+            tj[d] = r;
+            tx[d] = x[k];
+        }
+    free(next);
+}
+
+/* out = M v for CSR M with `rows` rows: out_r = sum_k M_rk v_k (in storage order). */
+void orc_spmv(int32_t rows, const int32_t *p, const int32_t *j, const double *x,
+              const double *v, double *out)
+{
+    for (int32_t r = 0; r < rows; ++r) {
+        double s = 0.0;
+        for (int64_t k = p[r]; k < p[r + 1]; ++k) s += x[k] * v[j[k]];
+        out[r] = s;
+    }
+}
+
+double orc_norm2(int64_t n, const double *v)
+{
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += v[i] * v[i];
+    return sqrt(s);
+}
+
+static double dot(int64_t n, const double *a, const double *b)
+{
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+}
+
+static double now_s(void)
+{
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
+/* ------------------------------------------------------- residuals, score */
+
+/* KKT score of (x, y) for objective c and bounds [l, u] (S-3, S-6):
+ *   z = c - A^T y;  r_P = b - A x
+ *   r_D_j = z_j - [l_j > -inf] max(z_j,0) + [u_j < inf] max(-z_j,0)  (violation part)
+ *   pobj = c^T x;  dobj = b^T y + sum_{l_j>-inf} l_j max(z_j,0) - sum_{u_j<inf} u_j max(-z_j,0)
+ *   score = max(||r_P||/(1+||b||), ||r_D||/(1+||c||), |pobj-dobj|/(1+|pobj|+|dobj|)) */
+void orc_score(const orc_lp *lp, const double *c, const double *l, const double *u,
+               double nb, double nc, const double *x, const double *y, orc_score_t *out)
+{
+    int32_t m = lp->m, n = lp->n;
+    double *ax = (double *)malloc(sizeof(double) * (m ? m : 1));
+    double *aty = (double *)malloc(sizeof(double) * (n ? n : 1));
+    orc_spmv(m, lp->Ap, lp->Aj, lp->Ax, x, ax);
+    orc_spmv(n, lp->ATp, lp->ATj, lp->ATx, y, aty);
+    double rp2 = 0.0;
+    for (int32_t i = 0; i < m; ++i) {
+        double r = lp->b[i] - ax[i];
+        rp2 += r * r;
+    }
+    double rd2 = 0.0, pobj = 0.0, bound_terms = 0.0;
+    for (int32_t j = 0; j < n; ++j) {
+        double z = c[j] - aty[j];
+        double zp = z > 0.0 ? z : 0.0;
+        double zm = -z > 0.0 ? -z : 0.0;
+        double rd = z;
+        if (l[j] > -INFINITY) { rd -= zp; bound_terms += l[j] * zp; }
+        if (u[j] < INFINITY)  { rd += zm; bound_terms -= u[j] * zm; }
+        rd2 += rd * rd;
+        pobj += c[j] * x[j];
+    }
+    double dobj = dot(m, lp->b, y) + bound_terms;
+    out->rp = sqrt(rp2);
+    out->rd = sqrt(rd2);
+    out->pobj = pobj;
+    out->dobj = dobj;
+    out->r_p = out->rp / (1.0 + nb);
+    out->r_d = out->rd / (1.0 + nc);
+    out->r_g = fabs(pobj - dobj) / (1.0 + fabs(pobj) + fabs(dobj));
+    double s = out->r_p;
+    if (out->r_d > s) s = out->r_d;
+    if (out->r_g > s) s = out->r_g;
+    out->score = s;
+    free(ax);
+    free(aty);
+}
+
+/* Operator-norm estimate (S-2): v0_j = U(seed,j) - 0.5, normalised; K power
+ * iterations v <- A^T A v / ||A^T A v||; sigma_hat = sqrt(||A^T A v||) at the last. */
+double orc_power_sigma(const orc_lp *lp, int32_t iters, uint64_t seed)
+{
+    int32_t m = lp->m, n = lp->n;
+    double *v = (double *)malloc(sizeof(double) * (n ? n : 1));
+    double *w = (double *)malloc(sizeof(double) * (m ? m : 1));
+    double *u = (double *)malloc(sizeof(double) * (n ? n : 1));
+    for (int32_t j = 0; j < n; ++j) v[j] = orc_u01(seed, j) - 0.5;
+    double nv = orc_norm2(n, v);
+    for (int32_t j = 0; j < n; ++j) v[j] = v[j] / nv;
+    double nu = 0.0;
+    for (int32_t it = 0; it < iters; ++it) {
+        orc_spmv(m, lp->Ap, lp->Aj, lp->Ax, v, w);
+        orc_spmv(n, lp->ATp, lp->ATj, lp->ATx, w, u);
+        nu = orc_norm2(n, u);
+        if (!(nu > 0.0)) break;
+        for (int32_t j = 0; j < n; ++j) v[j] = u[j] / nu;
+    }
+    free(v); free(w); free(u);
+    return sqrt(nu);
+}
+
+/* ------------------------------------------------------------------ R-PDHG */
+typedef struct {
+    const orc_lp *lp;
+    orc_params prm;
+    const double *c, *l, *u;   /* objective and bounds in use (M or M^) */
+    int mode;                  /* MODE_* */
+    double target;             /* primal-only: ||b - Ax|| <= target */
+    int64_t min_iters;
+    double nb, nc, eta, omega;
+    double *x, *y, *xavg, *yavg, *xr, *yr, *xn, *yn, *aty, *xbar, *axbar;
+    int64_t k, t, restarts;
+    double S_r, S_prev;
+    int status, returned_average;
+    double t0;
+} orc_state;
+
+void orc_destroy(orc_state *s)
+{
+    if (!s) return;
+    free(s->x); free(s->y); free(s->xavg); free(s->yavg); free(s->xr); free(s->yr);
+    free(s->xn); free(s->yn); free(s->aty); free(s->xbar); free(s->axbar);
+    free(s);
+}
+
+static double score_of(orc_state *s, const double *x, const double *y, orc_score_t *o)
+{
+    orc_score(s->lp, s->c, s->l, s->u, s->nb, s->nc, x, y, o);
+    return o->score;
+}
+
+static double proj(double v, double lo, double hi)
+{
+    double r = v > lo ? v : lo;   /* max(v, lo) */
+    return r < hi ? r : hi;       /* min(., hi) */
+}
+
+/* Create a run of R-PDHG on (A, b, c, [l,u]) (SURVEY §8(c) "Setup").
+ * eta_in > 0 overrides prm->step_size / power iteration; omega_in > 0 overrides
+ * prm->primal_weight.  x_init/y_init NULL => 0. */
+orc_state *orc_create(const orc_lp *lp, const orc_params *prm, const double *c,
+                      const double *l, const double *u, const double *x_init,
+                      const double *y_init, int mode, double target, int64_t min_iters,
+                      double eta_in)
+{
+    int32_t m = lp->m, n = lp->n;
+    orc_state *s = (orc_state *)calloc(1, sizeof(orc_state));
+    size_t N = (size_t)(n ? n : 1), M = (size_t)(m ? m : 1);
+    s->lp = lp; s->prm = *prm; s->c = c; s->l = l; s->u = u;
+    s->mode = mode; s->target = target; s->min_iters = min_iters;
+    s->x = (double *)calloc(N, 8); s->xavg = (double *)calloc(N, 8);
+    s->xr = (double *)calloc(N, 8); s->xn = (double *)calloc(N, 8);
+    s->aty = (double *)calloc(N, 8); s->xbar = (double *)calloc(N, 8);
+    s->y = (double *)calloc(M, 8); s->yavg = (double *)calloc(M, 8);
+    s->yr = (double *)calloc(M, 8); s->yn = (double *)calloc(M, 8);
+    s->axbar = (double *)calloc(M, 8);
+    s->t0 = now_s();
+    s->nb = orc_norm2(m, lp->b);
+    s->nc = orc_norm2(n, c);
+    if (eta_in > 0.0) s->eta = eta_in;
+    else if (prm->step_size > 0.0) s->eta = prm->step_size;
+    else s->eta = prm->step_scale / orc_power_sigma(lp, prm->power_iters, prm->seed);
+    if (prm->primal_weight > 0.0) s->omega = prm->primal_weight;
+    else s->omega = (s->nc > 1e-10 && s->nb > 1e-10) ? s->nc / s->nb : 1.0;
+    for (int32_t j = 0; j < n; ++j) s->x[j] = proj(x_init ? x_init[j] : 0.0, l[j], u[j]);
+    for (int32_t i = 0; i < m; ++i) s->y[i] = y_init ? y_init[i] : 0.0;
+    memcpy(s->xr, s->x, N * 8);
+    memcpy(s->yr, s->y, M * 8);
+    orc_score_t o;
+    s->S_r = score_of(s, s->x, s->y, &o);
+    s->S_prev = INFINITY;
+    s->k = 0; s->t = 0; s->restarts = 0;
+    s->status = -1; s->returned_average = 0;
+    if (mode == MODE_FULL && s->S_r <= prm->eps_rel) s->status = 0;
+    return s;
+}
+
+double orc_get_eta(const orc_state *s) { return s->eta; }
+double orc_get_omega(const orc_state *s) { return s->omega; }
+int64_t orc_get_k(const orc_state *s) { return s->k; }
+
+static double primal_res(orc_state *s, const double *x)
+{
+    const orc_lp *lp = s->lp;
+    orc_spmv(lp->m, lp->Ap, lp->Aj, lp->Ax, x, s->axbar);
+    double r2 = 0.0;
+    for (int32_t i = 0; i < lp->m; ++i) {
+        double r = lp->b[i] - s->axbar[i];
+        r2 += r * r;
+    }
+    return sqrt(r2);
+}
+
+/* Run up to `steps` more iterations (SURVEY §8(c) "loop"); returns status
+ * (-1 = still running after `steps`). */
+int orc_run(orc_state *s, int64_t steps)
+{
+    const orc_lp *lp = s->lp;
+    int32_t m = lp->m, n = lp->n;
+    const orc_params *P = &s->prm;
+    for (int64_t it = 0; it < steps && s->status < 0; ++it) {
+        double tau = s->eta / s->omega;
+        double sigma = s->eta * s->omega;
+        /* x+ = proj(x - tau (c - A^T y)) */
+        orc_spmv(n, lp->ATp, lp->ATj, lp->ATx, s->y, s->aty);
+        for (int32_t j = 0; j < n; ++j)
+            s->xn[j] = proj(s->x[j] - tau * (s->c[j] - s->aty[j]), s->l[j], s->u[j]);
+        /* y+ = y + sigma (b - A (2 x+ - x)) */
+        for (int32_t j = 0; j < n; ++j) s->xbar[j] = 2.0 * s->xn[j] - s->x[j];
+        orc_spmv(m, lp->Ap, lp->Aj, lp->Ax, s->xbar, s->axbar);
+        for (int32_t i = 0; i < m; ++i) s->yn[i] = s->y[i] + sigma * (lp->b[i] - s->axbar[i]);
+        int bad = 0;
+        for (int32_t j = 0; j < n; ++j) bad |= !isfinite(s->xn[j]);
+        for (int32_t i = 0; i < m; ++i) bad |= !isfinite(s->yn[i]);
+        if (bad) { s->status = 3; s->k += 1; break; }
+        s->t += 1;
+        for (int32_t j = 0; j < n; ++j) s->xavg[j] += (s->xn[j] - s->xavg[j]) / (double)s->t;
+        for (int32_t i = 0; i < m; ++i) s->yavg[i] += (s->yn[i] - s->yavg[i]) / (double)s->t;
+        memcpy(s->x, s->xn, sizeof(double) * n);
+        memcpy(s->y, s->yn, sizeof(double) * m);
+        s->k += 1;
+        orc_score_t o;
+        if (s->mode == MODE_FULL) {
+            if (score_of(s, s->x, s->y, &o) <= P->eps_rel) { s->status = 0; break; }
+        } else if (s->mode == MODE_PRIMAL_ONLY) {
+            if (s->k >= s->min_iters && primal_res(s, s->x) <= s->target) { s->status = 0; break; }
+        }
+        if (P->restart && s->t % P->check_every == 0) {
+            double S_a = score_of(s, s->xavg, s->yavg, &o);
+            double S_c = score_of(s, s->x, s->y, &o);
+            if (s->mode == MODE_FULL && S_a <= P->eps_rel) {
+                s->status = 0; s->returned_average = 1; break;
+            }
+            int use_avg = S_a < S_c;                       /* tie -> current (S-14) */
+            const double *xc = use_avg ? s->xavg : s->x;
+            const double *yc = use_avg ? s->yavg : s->y;
+            double S = use_avg ? S_a : S_c;
+            if (S <= P->beta_suff * s->S_r ||
+                (S <= P->beta_nec * s->S_r && S > s->S_prev) ||
+                (double)s->t >= P->beta_art * (double)s->k) {
+                double dx2 = 0.0, dy2 = 0.0;
+                for (int32_t j = 0; j < n; ++j) { double d = xc[j] - s->xr[j]; dx2 += d * d; }
+                for (int32_t i = 0; i < m; ++i) { double d = yc[i] - s->yr[i]; dy2 += d * d; }
+                double dx = sqrt(dx2), dy = sqrt(dy2);
+                if (dx > 1e-10 && dy > 1e-10)
+                    s->omega = exp(P->theta * log(dy / dx) + (1.0 - P->theta) * log(s->omega));
+                if (use_avg) {
+                    memcpy(s->x, s->xavg, sizeof(double) * n);
+                    memcpy(s->y, s->yavg, sizeof(double) * m);
+                }
+                memcpy(s->xr, s->x, sizeof(double) * n);
+                memcpy(s->yr, s->y, sizeof(double) * m);
+                s->S_r = S;
+                s->S_prev = INFINITY;
+                s->t = 0;
+                memset(s->xavg, 0, sizeof(double) * n);
+                memset(s->yavg, 0, sizeof(double) * m);
+                s->restarts += 1;
+            } else {
+                s->S_prev = S;
+            }
+        }
+        if (s->mode != MODE_NONE) {
+            if (s->k == P->max_iters) { s->status = 1; break; }
+            if (P->time_limit_s > 0.0 && now_s() - s->t0 > P->time_limit_s) { s->status = 2; break; }
+        }
+    }
+    return s->status;
+}
+
+/* The iterate a finished run returns (current, or the average when the average
+ * satisfied the tolerance at a check). */
+void orc_get(const orc_state *s, double *x, double *y)
+{
+    const double *xs = s->returned_average ? s->xavg : s->x;
+    const double *ys = s->returned_average ? s->yavg : s->y;
+    if (x) memcpy(x, xs, sizeof(double) * s->lp->n);
+    if (y) memcpy(y, ys, sizeof(double) * s->lp->m);
+}
+
+void orc_result_of(orc_state *s, orc_result *r)
+{
+    double *x = (double *)malloc(sizeof(double) * (s->lp->n ? s->lp->n : 1));
+    double *y = (double *)malloc(sizeof(double) * (s->lp->m ? s->lp->m : 1));
+    orc_get(s, x, y);
+    orc_score_t o;
+    score_of(s, x, y, &o);
+    r->status = s->status;
+    r->returned_average = s->returned_average;
+    r->iterations = s->k;
+    r->restarts = s->restarts;
+    r->pobj = o.pobj; r->dobj = o.dobj; r->gap = fabs(o.pobj - o.dobj);
+    r->rp_norm = o.rp; r->rd_norm = o.rd; r->score = o.score;
+    r->step_size = s->eta; r->primal_weight = s->omega;
+    r->wall_s = now_s() - s->t0;
+    free(x); free(y);
+}
+
+/* ----------------------------------------------------- Algorithm 1 */
+
+/* z = c - A^T y ("reduced costs"). */
+void orc_reduced_costs(const orc_lp *lp, const double *c, const double *y, double *z)
+{
+    orc_spmv(lp->n, lp->ATp, lp->ATj, lp->ATx, y, z);
+    for (int32_t j = 0; j < lp->n; ++j) z[j] = c[j] - z[j];
+}
+
+/* Corner model M^ (Algorithm 1 line 2):
+ *   lb^_j = x_j if z_j < -eps_abs else lb_j;  ub^_j = x_j if z_j > eps_abs else ub_j;
+ *   obj_j = obj_scale * U(seed, j)  (Uniform[0,1]^n; obj_scale P:771-779, S-12).
+ * chat may be NULL (caller supplies the objective). */
+void orc_corner_model(int32_t n, const double *x, const double *z, const double *l,
+                      const double *u, double eps_abs, double obj_scale, uint64_t seed,
+                      double *lhat, double *uhat, double *chat, int64_t *fix_lb, int64_t *fix_ub)
+{
+    int64_t fl = 0, fu = 0;
+    for (int32_t j = 0; j < n; ++j) {
+        if (z[j] < -eps_abs) { lhat[j] = x[j]; fl++; } else lhat[j] = l[j];
+        if (z[j] > eps_abs)  { uhat[j] = x[j]; fu++; } else uhat[j] = u[j];
+        if (chat) chat[j] = obj_scale * orc_u01(seed, j);
+    }
+    *fix_lb = fl;
+    *fix_ub = fu;
+}
+
+/* Off-bound test (Fig. 1 axis P:336; S-10): strictly inside by > tol
+ * on both sides; an infinite bound never counts as "at bound". */
+static int off_bound(double x, double lo, double hi, double tol)
+{
+    return (x - lo > tol) && (hi - x > tol);
+}
+
+/* Corner statistics a10 (S-9):
+ *   p = #off-bound (tol eps_abs, bounds [l,u]); p_strict (tol 0); p^ w.r.t. [l^,u^];
+ *   d = #{|z_j| <= eps_abs};  cand = #{off_j and |z_j| < eps_abs};
+ *   est_primal = max(p - m, 0); est_dual = max(m - d, 0);
+ *   candidate <=> cand >= max(2m, floor). z and lhat/uhat may be NULL. */
+void orc_stats(int32_t m, int32_t n, const double *x, const double *z, const double *l,
+               const double *u, const double *lhat, const double *uhat, double eps_abs,
+               int64_t floor_, orc_stats_t *st)
+{
+    memset(st, 0, sizeof(*st));
+    for (int32_t j = 0; j < n; ++j) {
+        int off = off_bound(x[j], l[j], u[j], eps_abs);
+        st->off_bound += off;
+        st->off_bound_strict += off_bound(x[j], l[j], u[j], 0.0);
+        if (lhat && uhat) st->off_bound_model += off_bound(x[j], lhat[j], uhat[j], eps_abs);
+        if (z) {
+            st->zero_rc += fabs(z[j]) <= eps_abs;
+            st->candidates += off && fabs(z[j]) < eps_abs;
+        }
+    }
+    st->est_primal_pushes = st->off_bound > m ? st->off_bound - m : 0;
+    st->est_dual_pushes = z ? (m > st->zero_rc ? m - st->zero_rc : 0) : 0;
+    int64_t thr = 2 * (int64_t)m > floor_ ? 2 * (int64_t)m : floor_;
+    st->is_candidate = z ? st->candidates >= thr : 0;
+}
