@@ -1,0 +1,143 @@
+// internal.cuh — host-side structures of libcpd (problem, solver, execution context).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cpd.h"
+#include "kernels.cuh"
+
+namespace cpd {
+
+// Error carried across the internal layers; converted to a cpd_error code at the ABI.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CPD_CUDA(call)                                                                         \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            throw ::cpd::Error(e_ == cudaErrorMemoryAllocation ? CPD_E_NOMEM : CPD_E_CUDA,     \
+                               std::string(#call) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+// Device buffer with RAII.
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    void alloc(size_t count)
+    {
+        free();
+        n = count;
+        if (count) CPD_CUDA(cudaMalloc(&p, sizeof(T) * count));
+    }
+    void free()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DBuf() { free(); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept
+    {
+        if (this != &o) {
+            free();
+            p = o.p; n = o.n; o.p = nullptr; o.n = 0;
+        }
+        return *this;
+    }
+};
+
+// nnz-balanced SpMV plan of one CSR layout (immutable, shared by solvers).
+struct Plan {
+    DBuf<PlanEntry> ent;
+    DBuf<int64_t> long_off;
+    int32_t nent = 0, nlong = 0;
+    int64_t chunks = 0;
+    int64_t stream_entries = 0, long_entries = 0;
+};
+void build_plan(int32_t rows, const std::vector<int32_t>& rowptr, Plan& plan);
+
+struct Matrix {
+    DBuf<int32_t> p, j;
+    DBuf<double> x;
+    int32_t rows = 0, cols = 0;
+    Plan plan;
+    DevCsr dev() const { return DevCsr{p.p, j.p, x.p, rows}; }
+};
+
+}  // namespace cpd
+
+struct cpd_problem {
+    int device = 0;
+    int32_t m = 0, n = 0;
+    int64_t nnz = 0;
+    cpd::Matrix A, AT;
+    cpd::DBuf<double> b, c, lb, ub;
+    bool uniform_bounds = false;
+    double l0 = 0.0, u0 = 0.0;
+    int num_sms = 148;
+    cpd::Bounds bounds() const
+    {
+        if (uniform_bounds) return cpd::Bounds{nullptr, nullptr, l0, u0};
+        return cpd::Bounds{lb.p, ub.p, 0.0, 0.0};
+    }
+};
+
+namespace cpd {
+
+// Per-stream execution context: control block, reduction scratch, long-row
+// scratch for both layouts.
+struct Ctx {
+    const cpd_problem* P = nullptr;
+    cudaStream_t st = nullptr;
+    DBuf<Ctl> ctl_main, ctl_aux;      // run control block / scratch block for one-off evaluations
+    Ctl* h_main = nullptr;           // pinned mirrors
+    Ctl* h_aux = nullptr;
+    Ctl* ctl = nullptr;              // active block (main unless an AuxScope is open)
+    Ctl* h_ctl = nullptr;
+    DBuf<double> bpart;
+    DBuf<unsigned> ctr;
+    DBuf<int32_t> lcntA, lcntAT;
+    DBuf<double> lpartA, laccA, lpartAT, laccAT;
+    int grid_elem = 0;
+    explicit Ctx(const cpd_problem* p);
+    ~Ctx();
+    DevPlan planA() const;
+    DevPlan planAT() const;
+    void pull_ctl();                                   // D2H of the control block + sync
+    void set_i64(int64_t* dev_field, int64_t v);
+    void set_i32(int32_t* dev_field, int32_t v);
+    void push_ctl(const Ctl& h);                      // H2D of a whole control block
+    void sync();
+    template <class F>
+    int grid_for(F kernel);
+};
+
+// Launch helpers (templates instantiated in solver.cu).
+// Switches a Ctx to its auxiliary control block for the scope's lifetime, so
+// one-off evaluations never disturb the state of a run in progress.
+struct AuxScope {
+    Ctx& cx;
+    explicit AuxScope(Ctx& c) : cx(c) { cx.ctl = cx.ctl_aux.p; cx.h_ctl = cx.h_aux; }
+    ~AuxScope() { cx.ctl = cx.ctl_main.p; cx.h_ctl = cx.h_main; }
+};
+
+template <int NV, class Epi>
+void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel v1, const Epi& epi,
+                 Gate g);
+template <class Op>
+void launch_elem(Ctx& cx, int64_t N, const Op& op, Gate g);
+
+}  // namespace cpd

@@ -1,0 +1,1002 @@
+// solver.cu — the R-PDHG run state machine,
+// Algorithm 1 orchestration, statistics, stand-alone entry points and
+// the extern "C" ABI of include/cpd.h.
+//
+// One run = begin (power iteration, norms, projected start, initial KKT) + batches.
+// A batch is the fixed node sequence
+//     [check A^T pass] [check A pass + decision] [restart apply] (K1_s, K2_s) s = 0..K-1
+// launched as ONE CUDA graph; every node reads the device control block and
+// either does its work or returns at once (gates), so the same graph serves every
+// batch and the host synchronises once per K iterations.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace cpd {
+
+// ------------------------------------------------------------------ Ctx
+Ctx::Ctx(const cpd_problem* p) : P(p)
+{
+    CPD_CUDA(cudaSetDevice(p->device));
+    CPD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    ctl_main.alloc(1);
+    ctl_aux.alloc(1);
+    CPD_CUDA(cudaMemset(ctl_main.p, 0, sizeof(Ctl)));
+    CPD_CUDA(cudaMemset(ctl_aux.p, 0, sizeof(Ctl)));
+    CPD_CUDA(cudaMallocHost(&h_main, sizeof(Ctl)));
+    CPD_CUDA(cudaMallocHost(&h_aux, sizeof(Ctl)));
+    std::memset(h_main, 0, sizeof(Ctl));
+    std::memset(h_aux, 0, sizeof(Ctl));
+    ctl = ctl_main.p;
+    h_ctl = h_main;
+    bpart.alloc((size_t)p->num_sms * 8 * NSMAX);
+    ctr.alloc(1);
+    CPD_CUDA(cudaMemset(ctr.p, 0, sizeof(unsigned)));
+    const Plan& pa = p->A.plan;
+    const Plan& pt = p->AT.plan;
+    lcntA.alloc(std::max(1, pa.nlong));
+    lcntAT.alloc(std::max(1, pt.nlong));
+    CPD_CUDA(cudaMemset(lcntA.p, 0, sizeof(int32_t) * lcntA.n));
+    CPD_CUDA(cudaMemset(lcntAT.p, 0, sizeof(int32_t) * lcntAT.n));
+    lpartA.alloc(std::max<int64_t>(1, pa.chunks * 2));
+    lpartAT.alloc(std::max<int64_t>(1, pt.chunks * 2));
+    laccA.alloc((size_t)std::max(1, pa.nlong) * NSMAX);
+    laccAT.alloc((size_t)std::max(1, pt.nlong) * NSMAX);
+    grid_elem = p->num_sms * 4;
+}
+
+Ctx::~Ctx()
+{
+    if (h_main) cudaFreeHost(h_main);
+    if (h_aux) cudaFreeHost(h_aux);
+    if (st) cudaStreamDestroy(st);
+}
+
+DevPlan Ctx::planA() const
+{
+    const Plan& pl = P->A.plan;
+    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.long_off.p, lcntA.p, lpartA.p, laccA.p};
+}
+
+DevPlan Ctx::planAT() const
+{
+    const Plan& pl = P->AT.plan;
+    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.long_off.p, lcntAT.p, lpartAT.p, laccAT.p};
+}
+
+void Ctx::pull_ctl()
+{
+    CPD_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CPD_CUDA(cudaStreamSynchronize(st));
+}
+
+void Ctx::push_ctl(const Ctl& h)
+{
+    *h_ctl = h;
+    CPD_CUDA(cudaMemcpyAsync(ctl, h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    CPD_CUDA(cudaStreamSynchronize(st));
+}
+
+__global__ void k_set_i64(int64_t* f, int64_t v) { *f = v; }
+__global__ void k_set_i32(int32_t* f, int32_t v) { *f = v; }
+
+void Ctx::set_i64(int64_t* f, int64_t v)
+{
+    k_set_i64<<<1, 1, 0, st>>>(f, v);
+    CPD_CUDA(cudaGetLastError());
+}
+
+void Ctx::set_i32(int32_t* f, int32_t v)
+{
+    k_set_i32<<<1, 1, 0, st>>>(f, v);
+    CPD_CUDA(cudaGetLastError());
+}
+
+void Ctx::sync() { CPD_CUDA(cudaStreamSynchronize(st)); }
+
+static std::mutex g_grid_mu;
+
+template <int NV, class Epi>
+void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel v1, const Epi& epi,
+                 Gate g)
+{
+    static int grid = 0, sms = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_grid_mu);
+        if (!grid || sms != cx.P->num_sms) {
+            int nb = 0;
+            CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spmv<NV, Epi>, TPB, 0));
+            nb = std::max(1, std::min(nb, 8));
+            sms = cx.P->num_sms;
+            grid = nb * sms;
+        }
+    }
+    const int gr = std::max(1, std::min(grid, dp.nent));
+    k_spmv<NV, Epi><<<gr, TPB, 0, cx.st>>>(M.dev(), dp, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p);
+    CPD_CUDA(cudaGetLastError());
+}
+
+template <class Op>
+void launch_elem(Ctx& cx, int64_t N, const Op& op, Gate g)
+{
+    const int64_t need = (N + TPB - 1) / TPB;
+    const int gr = (int)std::max<int64_t>(1, std::min<int64_t>(need, cx.grid_elem));
+    k_elem<Op><<<gr, TPB, 0, cx.st>>>(N, op, g, cx.ctl, cx.bpart.p, cx.ctr.p);
+    CPD_CUDA(cudaGetLastError());
+}
+
+static Gate always() { return Gate{GATE_ALWAYS, 0, 0, nullptr}; }
+static VecSel fixed(const double* v) { return VecSel{v, v, 0}; }
+static VecSel none() { return VecSel{nullptr, nullptr, 0}; }
+
+// Standalone evaluations shared by the solver and the stand-alone ABI calls.
+// score of (x, y) for objective c / bounds bd -> cx.h_ctl->last (after pull)
+static void eval_score(Ctx& cx, const double* x, const double* y, const double* c, Bounds bd,
+                       double nb, double nc, double out[8])
+{
+    AuxScope aux(cx);
+    const cpd_problem* P = cx.P;
+    Ctl h{};
+    h.nb = nb;
+    h.nc = nc;
+    h.K = 1;
+    cx.push_ctl(h);
+    EpiInitM em{P->b.p, y, nullptr};
+    launch_spmv<1>(cx, P->A, cx.planA(), fixed(x), none(), em, always());
+    EpiInitN en{c, x, bd, 0};
+    launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(y), none(), en, always());
+    cx.pull_ctl();
+    for (int i = 0; i < 8; ++i) out[i] = cx.h_ctl->last[i];
+}
+
+static void eval_norms(Ctx& cx, const double* b, const double* c, double* nb, double* nc)
+{
+    AuxScope aux(cx);
+    const cpd_problem* P = cx.P;
+    Ctl h{};
+    h.K = 1;
+    h.mode = MODE_NONE;
+    h.eta = 1.0;
+    cx.push_ctl(h);
+    OpNorms on{b, c, P->n, P->m, 1.0};
+    launch_elem(cx, std::max<int64_t>(P->n, P->m), on, always());
+    cx.pull_ctl();
+    *nb = cx.h_ctl->nb;
+    *nc = cx.h_ctl->nc;
+}
+
+static void eval_stats(Ctx& cx, const double* x, const double* z, const double* lh, const double* uh,
+                       double eps, int64_t floor_, int64_t fix_lb, int64_t fix_ub, cpd_stats* out)
+{
+    AuxScope aux(cx);
+    const cpd_problem* P = cx.P;
+    Ctl h{};
+    h.K = 1;
+    cx.push_ctl(h);
+    OpStats os{x, z, lh, uh, P->bounds(), eps};
+    launch_elem(cx, P->n, os, always());
+    cx.pull_ctl();
+    const double* o = cx.h_ctl->out;
+    std::memset(out, 0, sizeof(*out));
+    out->off_bound = (int64_t)o[0];
+    out->off_bound_strict = (int64_t)o[1];
+    out->off_bound_model = lh ? (int64_t)o[2] : 0;
+    out->zero_rc = z ? (int64_t)o[3] : 0;
+    out->candidates = z ? (int64_t)o[4] : 0;
+    out->fix_lb = fix_lb;
+    out->fix_ub = fix_ub;
+    const int64_t m = P->m;
+    out->est_primal_pushes = std::max<int64_t>(out->off_bound - m, 0);
+    out->est_dual_pushes = z ? std::max<int64_t>(m - out->zero_rc, 0) : 0;
+    const int64_t thr = std::max<int64_t>(2 * m, floor_);
+    out->is_candidate = z ? (out->candidates >= thr) : 0;
+}
+
+static double power_sigma(Ctx& cx, int32_t iters, uint64_t seed, double step_scale, double* v,
+                          double* w)
+{
+    AuxScope aux(cx);
+    const cpd_problem* P = cx.P;
+    Ctl h{};
+    h.K = 1;
+    h.step_scale = step_scale;
+    cx.push_ctl(h);
+    OpPowInit pi{v, seed, P->n};
+    launch_elem(cx, P->n, pi, always());
+    for (int it = 0; it < iters; ++it) {
+        EpiPowM pm{w, 0.0};
+        launch_spmv<1>(cx, P->A, cx.planA(), fixed(v), none(), pm, always());
+        EpiPowN pn{v};
+        launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(w), none(), pn, always());
+    }
+    cx.pull_ctl();
+    return cx.h_ctl->sigma_hat;
+}
+
+__global__ void k_copy(int64_t N, double* dst, const double* src)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+__global__ void k_zero(int64_t N, double* dst)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = 0.0;
+}
+
+// z = c - A^T y
+struct EpiZ {
+    static constexpr int NS = 1;
+    const double* c;
+    double* z;
+    __device__ void load(const Ctl*) {}
+    __device__ __forceinline__ void row(int j, const double* s, double*) const { z[j] = c[j] - s[0]; }
+    __device__ void finalize(const double*, Ctl*) const {}
+};
+
+}  // namespace cpd
+
+// ====================================================================== solver
+using namespace cpd;
+
+enum { NODE_CHECK_N = 0, NODE_CHECK_M = 1, NODE_RESTART = 2, NODE_K0 = 3 };
+enum { KT_K1 = 0, KT_K2 = 1, KT_CN = 2, KT_CM = 3, KT_RS = 4, KT_N = 5 };
+static const char* KT_NAMES[2][KT_N] = {
+    {"primal_step_AT", "dual_step_A", "check_eval_AT", "check_eval_A", "restart_apply"},
+    {"primal_step_AT:corner", "dual_step_A:corner", "check_eval_AT:corner", "check_eval_A:corner",
+     "restart_apply:corner"}};
+
+struct RunCfg {
+    int kind = 0;            // 0 original model, 1 corner model
+    int mode = MODE_FULL;
+    int64_t max_iters = 0, min_iters = 0;
+    double time_limit = 0.0;
+    const double* xs = nullptr;
+    const double* ys = nullptr;   // null => y = 0
+    bool power = false;
+    double eta = 0.0;
+    double omega_in = 0.0;
+    int traj = 0;
+};
+
+struct cpd_solver {
+    const cpd_problem* P;
+    cpd_params prm;
+    Ctx cx;
+    DBuf<double> X0, X1, Xa0, Xa1, Xr, Y, Ya, Yr, AX, AXa, Ystar, Z, lhat, uhat, chat, objd, SN, SM;
+    DBuf<int64_t> trk, troff;
+    DBuf<double> trrp;
+    DBuf<int32_t> active;
+    int32_t* h_active = nullptr;
+    int cur_par = 0;            // parity of the buffer holding the current x
+    bool run_active = false;
+    int run_kind = 0;
+    int64_t run_k_base = 0;
+    bool have_corner = false;
+    double eta_phase1 = 0.0;
+    bool eta_known = false;
+    int64_t fix_lb = 0, fix_ub = 0;
+    double corner_eps = 1e-6;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    cudaGraph_t graph[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev0, ev1;
+    double kt_ms[2][KT_N] = {};
+    int64_t kt_n[2][KT_N] = {};
+    int nnodes = 0;
+    const int64_t traj_cap = 1 << 16;
+
+    cpd_solver(const cpd_problem* p, const cpd_params& pr) : P(p), prm(pr), cx(p)
+    {
+        const size_t n = p->n, m = p->m;
+        for (auto* b : {&X0, &X1, &Xa0, &Xa1, &Xr, &Z, &lhat, &uhat, &chat, &objd, &SN}) b->alloc(n);
+        for (auto* b : {&Y, &Ya, &Yr, &AX, &AXa, &Ystar, &SM}) b->alloc(m);
+        for (auto* b : {&X0, &X1, &Xa0, &Xa1, &Xr, &Z}) CPD_CUDA(cudaMemset(b->p, 0, sizeof(double) * n));
+        for (auto* b : {&Y, &Ya, &Yr, &AX, &AXa, &Ystar}) CPD_CUDA(cudaMemset(b->p, 0, sizeof(double) * m));
+        trk.alloc(traj_cap);
+        troff.alloc(traj_cap);
+        trrp.alloc(traj_cap);
+        nnodes = NODE_K0 + 2 * prm.check_every;
+        active.alloc(nnodes);
+        CPD_CUDA(cudaMallocHost(&h_active, sizeof(int32_t) * nnodes));
+        if (prm.profile) {
+            ev0.resize(nnodes);
+            ev1.resize(nnodes);
+            for (int i = 0; i < nnodes; ++i) {
+                CPD_CUDA(cudaEventCreate(&ev0[i]));
+                CPD_CUDA(cudaEventCreate(&ev1[i]));
+            }
+        }
+        CPD_CUDA(cudaDeviceSynchronize());
+    }
+    ~cpd_solver()
+    {
+        for (int k = 0; k < 2; ++k) {
+            if (gexec[k]) cudaGraphExecDestroy(gexec[k]);
+            if (graph[k]) cudaGraphDestroy(graph[k]);
+        }
+        for (auto e : ev0) cudaEventDestroy(e);
+        for (auto e : ev1) cudaEventDestroy(e);
+        if (h_active) cudaFreeHost(h_active);
+    }
+    double* Xp(int par) { return par ? X1.p : X0.p; }
+
+    const double* obj_of(int kind) const { return kind ? chat.p : P->c.p; }
+    Bounds bounds_of(int kind) const
+    {
+        return kind ? Bounds{lhat.p, uhat.p, 0.0, 0.0} : P->bounds();
+    }
+
+    // ---------------------------------------------------------- begin
+    void begin(const RunCfg& rc)
+    {
+        const int32_t n = P->n, m = P->m;
+        Ctl h{};
+        h.mode = rc.mode;
+        h.restart_on = prm.restart ? 1 : 0;
+        h.K = prm.check_every;
+        h.traj_on = rc.traj;
+        h.k_stop = 0;
+        h.max_iters = rc.max_iters;
+        h.min_iters = rc.min_iters;
+        h.eps_rel = prm.eps_rel;
+        h.eps_abs = corner_eps;
+        h.beta_suff = prm.beta_suff;
+        h.beta_nec = prm.beta_nec;
+        h.beta_art = prm.beta_art;
+        h.theta = prm.theta;
+        h.status = ST_RUNNING;
+        h.eta = rc.eta;
+        h.step_scale = prm.step_scale;
+        h.S_prev = INFINITY;
+        h.traj_cap = traj_cap;
+        h.traj_k = trk.p;
+        h.traj_off = troff.p;
+        h.traj_rp = trrp.p;
+        cx.push_ctl(h);
+        if (rc.power) {
+            // power iteration into scratch (SN, SM); writes ctl->eta
+            OpPowInit pi{SN.p, prm.seed, n};
+            launch_elem(cx, n, pi, always());
+            for (int it = 0; it < prm.power_iters; ++it) {
+                EpiPowM pm{SM.p, 0.0};
+                launch_spmv<1>(cx, P->A, cx.planA(), fixed(SN.p), none(), pm, always());
+                EpiPowN pn{SN.p};
+                launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(SM.p), none(), pn, always());
+            }
+        }
+        const double* c = obj_of(rc.kind);
+        const Bounds bd = bounds_of(rc.kind);
+        OpNorms on{P->b.p, c, n, m, rc.omega_in};
+        launch_elem(cx, std::max(n, m), on, always());
+        OpBegin ob{rc.xs, rc.ys, bd, X0.p, Xa0.p, Xa1.p, Xr.p, Y.p, Ya.p, Yr.p, n, m, rc.ys ? 0 : 1};
+        launch_elem(cx, std::max(n, m), ob, always());
+        EpiInitM em{P->b.p, Y.p, AX.p};
+        launch_spmv<1>(cx, P->A, cx.planA(), fixed(X0.p), none(), em, always());
+        EpiInitN en{c, X0.p, bd, 1};
+        launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), en, always());
+        cx.pull_ctl();
+        cur_par = 0;
+        run_active = true;
+        run_kind = rc.kind;
+        if (!std::isfinite(cx.h_ctl->eta) || !(cx.h_ctl->eta > 0.0))
+            throw Error(CPD_E_ARG, "step size is not positive and finite (zero matrix?)");
+    }
+
+    // ---------------------------------------------------------- one batch
+    void enqueue_batch(int kind, bool capture)
+    {
+        const int32_t n = P->n, m = P->m;
+        const int K = prm.check_every;
+        const double* c = obj_of(kind);
+        const Bounds bd = bounds_of(kind);
+        const Bounds orig = P->bounds();
+        const PingPong X{{X0.p, X1.p}}, Xa{{Xa0.p, Xa1.p}};
+        auto rec = [&](std::vector<cudaEvent_t>& ev, int node) {
+            if (!prm.profile) return;
+            if (capture) CPD_CUDA(cudaEventRecordWithFlags(ev[node], cx.st, cudaEventRecordExternal));
+            else CPD_CUDA(cudaEventRecord(ev[node], cx.st));
+        };
+        CPD_CUDA(cudaMemsetAsync(active.p, 0, sizeof(int32_t) * nnodes, cx.st));
+        // restart check: A^T pass (current y and average y) + A pass (A x_avg) + decision
+        {
+            EpiCheckN e{c, bd, orig, X, Xa, Xr.p, prm.restart ? 1 : 0, 0.0, nullptr, nullptr, 0};
+            Gate g{GATE_CHECK, 0, NODE_CHECK_N, active.p};
+            rec(ev0, NODE_CHECK_N);
+            if (prm.restart)
+                launch_spmv<2>(cx, P->AT, cx.planAT(), fixed(Y.p), fixed(Ya.p), e, g);
+            else
+                launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), e, g);
+            rec(ev1, NODE_CHECK_N);
+            EpiCheckM em{P->b.p, Y.p, Ya.p, Yr.p, AXa.p};
+            Gate gm{GATE_CHECK, 0, NODE_CHECK_M, active.p};
+            rec(ev0, NODE_CHECK_M);
+            launch_spmv<1>(cx, P->A, cx.planA(), VecSel{Xa0.p, Xa1.p, 2}, none(), em, gm);
+            rec(ev1, NODE_CHECK_M);
+            OpRestart orr{X, Xa, Y.p, Ya.p, AX.p, AXa.p, Xr.p, Yr.p, n, m, 0, nullptr, nullptr};
+            Gate gr{GATE_RESTART, 0, NODE_RESTART, active.p};
+            rec(ev0, NODE_RESTART);
+            launch_elem(cx, std::max(n, m), orr, gr);
+            rec(ev1, NODE_RESTART);
+        }
+        for (int s = 0; s < K; ++s) {
+            const int n1 = NODE_K0 + 2 * s, n2 = n1 + 1;
+            EpiPrimal e1{c, bd, X, Xa, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr, 0.0};
+            rec(ev0, n1);
+            launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), e1, Gate{GATE_K1, s, n1, active.p});
+            rec(ev1, n1);
+            EpiDual e2{P->b.p, Y.p, Ya.p, AX.p, 0.0, 0.0};
+            rec(ev0, n2);
+            launch_spmv<1>(cx, P->A, cx.planA(), VecSel{X0.p, X1.p, 1}, none(), e2,
+                           Gate{GATE_K2, s, n2, active.p});
+            rec(ev1, n2);
+        }
+        CPD_CUDA(cudaMemcpyAsync(h_active, active.p, sizeof(int32_t) * nnodes, cudaMemcpyDeviceToHost, cx.st));
+        CPD_CUDA(cudaMemcpyAsync(cx.h_ctl, cx.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, cx.st));
+    }
+
+    void run_batch()
+    {
+        const int kind = run_kind;
+        if (prm.use_graph) {
+            if (!gexec[kind]) {
+                CPD_CUDA(cudaStreamBeginCapture(cx.st, cudaStreamCaptureModeThreadLocal));
+                try {
+                    enqueue_batch(kind, true);
+                } catch (...) {
+                    cudaGraph_t g;
+                    cudaStreamEndCapture(cx.st, &g);
+                    if (g) cudaGraphDestroy(g);
+                    throw;
+                }
+                CPD_CUDA(cudaStreamEndCapture(cx.st, &graph[kind]));
+                CPD_CUDA(cudaGraphInstantiate(&gexec[kind], graph[kind], 0));
+            }
+            CPD_CUDA(cudaGraphLaunch(gexec[kind], cx.st));
+        } else {
+            enqueue_batch(kind, false);
+        }
+        CPD_CUDA(cudaStreamSynchronize(cx.st));
+        if (prm.profile) account_times(kind);
+    }
+
+    void account_times(int kind)
+    {
+        for (int node = 0; node < nnodes; ++node) {
+            if (!h_active[node]) continue;
+            float ms = 0.f;
+            CPD_CUDA(cudaEventElapsedTime(&ms, ev0[node], ev1[node]));
+            int kt;
+            if (node == NODE_CHECK_N) kt = KT_CN;
+            else if (node == NODE_CHECK_M) kt = KT_CM;
+            else if (node == NODE_RESTART) kt = KT_RS;
+            else kt = ((node - NODE_K0) & 1) ? KT_K2 : KT_K1;
+            kt_ms[kind][kt] += ms;
+            kt_n[kind][kt] += 1;
+        }
+    }
+
+    // Advance the run until it terminates or reaches iteration k_stop.
+    void advance(int64_t k_stop, double time_limit)
+    {
+        cx.set_i64(&cx.ctl->k_stop, k_stop);
+        cx.pull_ctl();
+        const auto t0 = std::chrono::steady_clock::now();
+        while (true) {
+            const Ctl& h = *cx.h_ctl;
+            if (h.done) break;
+            if (h.k >= k_stop && !h.check_pending) break;
+            run_batch();
+            if (time_limit > 0.0 && !cx.h_ctl->done) {
+                const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                if (el > time_limit) {
+                    cx.set_i32(&cx.ctl->status, ST_TIME_LIMIT);
+                    cx.set_i64(&cx.ctl->iterations, cx.h_ctl->k);
+                    cx.set_i32(&cx.ctl->done, 1);
+                    cx.pull_ctl();
+                    break;
+                }
+            }
+        }
+        cur_par = (int)(cx.h_ctl->k & 1);
+    }
+
+    // After a terminated run: make (X[cur_par], Y) the returned point.
+    void commit()
+    {
+        const Ctl& h = *cx.h_ctl;
+        const int64_t k = h.k;
+        cur_par = (int)(k & 1);
+        if (h.returned_average) {
+            const int g = std::min<int64_t>(cx.grid_elem, ((int64_t)std::max(P->n, P->m) + 255) / 256);
+            k_copy<<<g, 256, 0, cx.st>>>(P->n, Xp(cur_par), (k & 1) ? Xa1.p : Xa0.p);
+            k_copy<<<g, 256, 0, cx.st>>>(P->m, Y.p, Ya.p);
+            CPD_CUDA(cudaGetLastError());
+        }
+        run_active = false;
+    }
+
+    void fill_result(cpd_result* r, int kind, double wall)
+    {
+        const Ctl h = *cx.h_ctl;   // state at termination
+        double o[8];
+        eval_score(cx, Xp(cur_par), Y.p, obj_of(kind), bounds_of(kind), h.nb, h.nc, o);
+        r->status = h.status;
+        r->returned_average = h.returned_average;
+        r->iterations = (h.status == ST_RUNNING) ? h.k : h.iterations;
+        r->restarts = h.restarts;
+        r->pobj = o[2];
+        r->dobj = o[3];
+        r->gap = std::fabs(o[2] - o[3]);
+        r->rp_norm = o[0];
+        r->rd_norm = o[1];
+        r->score = o[7];
+        r->step_size = h.eta;
+        r->primal_weight = h.omega;
+        r->wall_s = wall;
+    }
+
+    void solve(cpd_result* out)
+    {
+        const auto t0 = std::chrono::steady_clock::now();
+        RunCfg rc;
+        rc.kind = 0;
+        rc.mode = MODE_FULL;
+        rc.max_iters = prm.max_iters;
+        rc.xs = Xp(cur_par);
+        rc.ys = Y.p;
+        rc.power = !(prm.step_size > 0.0);
+        rc.eta = prm.step_size;
+        rc.omega_in = prm.primal_weight;
+        begin(rc);
+        eta_phase1 = cx.h_ctl->eta;
+        eta_known = true;
+        advance(prm.max_iters, prm.time_limit_s);
+        commit();
+        cx.sync();
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (out) fill_result(out, 0, wall);
+    }
+
+    void step(int64_t k)
+    {
+        if (!run_active || run_kind != 0) {
+            RunCfg rc;
+            rc.kind = 0;
+            rc.mode = MODE_NONE;
+            rc.max_iters = INT64_MAX;
+            rc.xs = Xp(cur_par);
+            rc.ys = Y.p;
+            rc.power = !(prm.step_size > 0.0);
+            rc.eta = prm.step_size;
+            rc.omega_in = prm.primal_weight;
+            begin(rc);
+            run_k_base = 0;
+        }
+        advance(cx.h_ctl->k + k, 0.0);
+    }
+
+    void corner_push(const cpd_corner_params& cp, cpd_result* out, cpd_stats* before, cpd_stats* after)
+    {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (run_active) commit();
+        const int32_t n = P->n, m = P->m;
+        corner_eps = cp.eps_abs;
+        const int g = std::min<int64_t>(cx.grid_elem, ((int64_t)std::max(n, m) + 255) / 256);
+        // phase-1 solution (x*, y*): x* stays in X[cur_par]; y* saved in Ystar
+        k_copy<<<g, 256, 0, cx.st>>>(m, Ystar.p, Y.p);
+        CPD_CUDA(cudaGetLastError());
+        const double* obj = nullptr;
+        if (cp.obj) {
+            CPD_CUDA(cudaMemcpyAsync(objd.p, cp.obj, sizeof(double) * n,
+                                     cp.obj_mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                     cx.st));
+            obj = objd.p;
+        }
+        // Algorithm 1 line 2: z*, bound map, objective
+        {
+            AuxScope aux(cx);
+            Ctl h{};
+            h.K = 1;
+            cx.push_ctl(h);
+            EpiCorner ec{P->c.p, Xp(cur_par), P->bounds(), Z.p, lhat.p, uhat.p, chat.p, obj, cp.eps_abs,
+                         cp.obj_scale, cp.seed};
+            launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Ystar.p), none(), ec, always());
+            cx.pull_ctl();
+            fix_lb = (int64_t)cx.h_ctl->out[0];
+            fix_ub = (int64_t)cx.h_ctl->out[1];
+        }
+        have_corner = true;
+        if (before)
+            eval_stats(cx, Xp(cur_par), Z.p, lhat.p, uhat.p, cp.eps_abs, cp.candidate_floor, fix_lb, fix_ub,
+                       before);
+        if (!eta_known) {
+            // no phase 1 on this solver: step size as phase 1 would have chosen it
+            if (prm.step_size > 0.0) eta_phase1 = prm.step_size;
+            else eta_phase1 = prm.step_scale / power_sigma(cx, prm.power_iters, prm.seed, 1.0, SN.p, SM.p);
+            eta_known = true;
+        }
+        RunCfg rc;
+        rc.kind = 1;
+        rc.mode = MODE_PRIMAL_ONLY;
+        rc.max_iters = cp.max_iters;
+        rc.min_iters = cp.min_iters;
+        rc.xs = Xp(cur_par);
+        rc.ys = nullptr;   // Algorithm 1 line 3: start from (x, 0)
+        rc.power = false;
+        rc.eta = eta_phase1;
+        rc.omega_in = 0.0;   // fresh primal weight from ||c^|| / ||b|| (S-8)
+        rc.traj = cp.traj_every > 0 ? 1 : 0;
+        begin(rc);
+        advance(cp.max_iters, cp.time_limit_s);
+        commit();
+        cx.sync();
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (out) fill_result(out, 1, wall);
+        // y, z returned are phase 1's
+        k_copy<<<g, 256, 0, cx.st>>>(m, Y.p, Ystar.p);
+        CPD_CUDA(cudaGetLastError());
+        if (after)
+            eval_stats(cx, Xp(cur_par), Z.p, lhat.p, uhat.p, cp.eps_abs, cp.candidate_floor, fix_lb, fix_ub,
+                       after);
+    }
+
+    void set_iterate(const double* x, const double* y, int mem)
+    {
+        const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        if (x) CPD_CUDA(cudaMemcpyAsync(X0.p, x, sizeof(double) * P->n, kind, cx.st));
+        else CPD_CUDA(cudaMemsetAsync(X0.p, 0, sizeof(double) * P->n, cx.st));
+        if (y) CPD_CUDA(cudaMemcpyAsync(Y.p, y, sizeof(double) * P->m, kind, cx.st));
+        else CPD_CUDA(cudaMemsetAsync(Y.p, 0, sizeof(double) * P->m, cx.st));
+        cx.sync();
+        cur_par = 0;
+        run_active = false;
+        have_corner = false;
+        eta_known = false;
+    }
+
+    void compute_z()
+    {
+        AuxScope aux(cx);
+        Ctl h{};
+        h.K = 1;
+        cx.push_ctl(h);
+        EpiZ ez{P->c.p, Z.p};
+        launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), ez, always());
+        cx.sync();
+    }
+
+    void get_iterate(double* x, double* y, double* z, int mem)
+    {
+        const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        if (z) compute_z();
+        if (x) CPD_CUDA(cudaMemcpyAsync(x, Xp(cur_par), sizeof(double) * P->n, kind, cx.st));
+        if (y) CPD_CUDA(cudaMemcpyAsync(y, Y.p, sizeof(double) * P->m, kind, cx.st));
+        if (z) CPD_CUDA(cudaMemcpyAsync(z, Z.p, sizeof(double) * P->n, kind, cx.st));
+        cx.sync();
+    }
+
+    double kernel_bytes(const std::string& name) const
+    {
+        const double nnz = (double)P->nnz, n = P->n, m = P->m;
+        const bool corner = name.find(":corner") != std::string::npos;
+        const std::string base = name.substr(0, name.find(':'));
+        const double bnd = (corner || !P->uniform_bounds) ? 16.0 * n : 0.0;
+        if (base == "primal_step_AT") return 12 * nnz + 4 * (n + 1) + 8 * m + 40 * n + bnd;
+        if (base == "dual_step_A") return 12 * nnz + 4 * (m + 1) + 8 * n + 56 * m;
+        if (base == "check_eval_AT")
+            return 12 * nnz + 4 * (n + 1) + (prm.restart ? 16 : 8) * m + 32 * n + bnd + (corner ? 16 * n : 0);
+        if (base == "check_eval_A") return 12 * nnz + 4 * (m + 1) + 8 * n + 40 * m;
+        if (base == "restart_apply") return 32 * n + 48 * m;
+        return -1.0;
+    }
+};
+
+// ====================================================================== ABI
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg)
+{
+    g_err = msg;
+    return code;
+}
+
+#define ABI_BEGIN try {
+#define ABI_END                                                                 \
+    }                                                                           \
+    catch (const cpd::Error& e) { return fail(e.code, e.what()); }              \
+    catch (const std::bad_alloc&) { return fail(CPD_E_NOMEM, "host allocation failed"); } \
+    catch (const std::exception& e) { return fail(CPD_E_CUDA, e.what()); }      \
+    catch (...) { return fail(CPD_E_CUDA, "unknown error"); }                   \
+    return CPD_OK;
+
+cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const int32_t* Ap,
+                                     const int32_t* Aj, const double* Ax, const int32_t* ATp,
+                                     const int32_t* ATj, const double* ATx, const double* b,
+                                     const double* c, const double* lb, const double* ub,
+                                     int32_t mem, int32_t device);
+
+extern "C" {
+
+const char* cpd_last_error(void) { return g_err.c_str(); }
+int cpd_version(void) { return CPD_VERSION; }
+
+int cpd_problem_create(int32_t m, int32_t n, int64_t nnz, const int32_t* A_rowptr, const int32_t* A_col,
+                       const double* A_val, const int32_t* AT_rowptr, const int32_t* AT_col,
+                       const double* AT_val, const double* b, const double* c, const double* lb,
+                       const double* ub, int32_t mem, int32_t device, cpd_problem** out)
+{
+    ABI_BEGIN
+    if (!out) return fail(CPD_E_ARG, "out is NULL");
+    *out = cpd_problem_create_impl(m, n, nnz, A_rowptr, A_col, A_val, AT_rowptr, AT_col, AT_val, b, c, lb,
+                                   ub, mem, device);
+    ABI_END
+}
+
+int cpd_problem_destroy(cpd_problem* p)
+{
+    ABI_BEGIN
+    if (p) {
+        cudaSetDevice(p->device);
+        delete p;
+    }
+    ABI_END
+}
+
+int cpd_problem_info(const cpd_problem* p, int64_t info[8])
+{
+    ABI_BEGIN
+    if (!p || !info) return fail(CPD_E_ARG, "NULL argument");
+    info[0] = p->m;
+    info[1] = p->n;
+    info[2] = p->nnz;
+    info[3] = p->A.plan.nlong;
+    info[4] = p->AT.plan.nlong;
+    info[5] = p->A.plan.nent;
+    info[6] = p->AT.plan.nent;
+    info[7] = p->uniform_bounds ? 1 : 0;
+    ABI_END
+}
+
+void cpd_params_default(cpd_params* p)
+{
+    if (!p) return;
+    std::memset(p, 0, sizeof(*p));
+    p->eps_rel = 1e-4;
+    p->eps_abs = 1e-6;
+    p->max_iters = 100000;
+    p->time_limit_s = 0.0;
+    p->check_every = 64;
+    p->step_scale = 0.9;
+    p->step_size = 0.0;
+    p->power_iters = 128;
+    p->seed = 7;
+    p->primal_weight = 0.0;
+    p->restart = 1;
+    p->beta_suff = 0.2;
+    p->beta_nec = 0.8;
+    p->beta_art = 0.36;
+    p->theta = 0.5;
+    p->use_graph = 1;
+    p->profile = 0;
+}
+
+void cpd_corner_params_default(cpd_corner_params* p)
+{
+    if (!p) return;
+    std::memset(p, 0, sizeof(*p));
+    p->eps_abs = 1e-6;
+    p->obj_scale = 1.0;
+    p->seed = 1001;
+    p->obj = nullptr;
+    p->obj_mem = CPD_HOST;
+    p->min_iters = 100;
+    p->max_iters = 100000;
+    p->time_limit_s = 0.0;
+    p->traj_every = 64;
+    p->candidate_floor = 100000;
+}
+
+int cpd_solver_create(const cpd_problem* p, const cpd_params* prm, cpd_solver** out)
+{
+    ABI_BEGIN
+    if (!p || !out) return fail(CPD_E_ARG, "NULL argument");
+    cpd_params d;
+    cpd_params_default(&d);
+    const cpd_params& pr = prm ? *prm : d;
+    if (pr.check_every < 1 || pr.check_every > 1024) return fail(CPD_E_ARG, "check_every must be in [1, 1024]");
+    if (!(pr.eps_rel > 0.0) || !(pr.step_scale > 0.0) || pr.power_iters < 1 || pr.max_iters < 0 ||
+        pr.restart < 0 || pr.restart > 1)
+        return fail(CPD_E_ARG, "invalid parameter");
+    CPD_CUDA(cudaSetDevice(p->device));
+    *out = new cpd_solver(p, pr);
+    ABI_END
+}
+
+int cpd_solver_destroy(cpd_solver* s)
+{
+    ABI_BEGIN
+    if (s) {
+        cudaSetDevice(s->P->device);
+        delete s;
+    }
+    ABI_END
+}
+
+int cpd_solve(cpd_solver* s, cpd_result* out)
+{
+    ABI_BEGIN
+    if (!s) return fail(CPD_E_ARG, "NULL solver");
+    CPD_CUDA(cudaSetDevice(s->P->device));
+    s->solve(out);
+    ABI_END
+}
+
+int cpd_corner_push(cpd_solver* s, const cpd_corner_params* cp, cpd_result* out, cpd_stats* before,
+                    cpd_stats* after)
+{
+    ABI_BEGIN
+    if (!s) return fail(CPD_E_ARG, "NULL solver");
+    cpd_corner_params d;
+    cpd_corner_params_default(&d);
+    const cpd_corner_params& c = cp ? *cp : d;
+    if (!(c.eps_abs >= 0.0) || c.min_iters < 0 || c.max_iters < 0) return fail(CPD_E_ARG, "invalid corner parameter");
+    CPD_CUDA(cudaSetDevice(s->P->device));
+    s->corner_push(c, out, before, after);
+    ABI_END
+}
+
+int cpd_step(cpd_solver* s, int64_t k)
+{
+    ABI_BEGIN
+    if (!s || k < 0) return fail(CPD_E_ARG, "NULL solver or k < 0");
+    CPD_CUDA(cudaSetDevice(s->P->device));
+    s->step(k);
+    ABI_END
+}
+
+int cpd_get_iterate(const cpd_solver* s, double* x, double* y, double* z, int32_t mem)
+{
+    ABI_BEGIN
+    if (!s) return fail(CPD_E_ARG, "NULL solver");
+    CPD_CUDA(cudaSetDevice(s->P->device));
+    const_cast<cpd_solver*>(s)->get_iterate(x, y, z, mem);
+    ABI_END
+}
+
+int cpd_set_iterate(cpd_solver* s, const double* x, const double* y, int32_t mem)
+{
+    ABI_BEGIN
+    if (!s) return fail(CPD_E_ARG, "NULL solver");
+    CPD_CUDA(cudaSetDevice(s->P->device));
+    s->set_iterate(x, y, mem);
+    ABI_END
+}
+
+int cpd_get_stats(const cpd_solver* cs, int64_t candidate_floor, cpd_stats* out)
+{
+    ABI_BEGIN
+    if (!cs || !out) return fail(CPD_E_ARG, "NULL argument");
+    auto* s = const_cast<cpd_solver*>(cs);
+    CPD_CUDA(cudaSetDevice(s->P->device));
+    s->compute_z();
+    eval_stats(s->cx, s->Xp(s->cur_par), s->Z.p, s->have_corner ? s->lhat.p : nullptr,
+               s->have_corner ? s->uhat.p : nullptr, s->have_corner ? s->corner_eps : s->prm.eps_abs,
+               candidate_floor, s->have_corner ? s->fix_lb : 0, s->have_corner ? s->fix_ub : 0, out);
+    ABI_END
+}
+
+int cpd_get_trajectory(const cpd_solver* s, int64_t* k, int64_t* off_bound, double* rp, int64_t cap,
+                       int64_t* len)
+{
+    ABI_BEGIN
+    if (!s || !len) return fail(CPD_E_ARG, "NULL argument");
+    CPD_CUDA(cudaSetDevice(s->P->device));
+    Ctl h;
+    CPD_CUDA(cudaMemcpy(&h, s->cx.ctl_main.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    const int64_t L = std::min<int64_t>(h.traj_len, std::max<int64_t>(cap, 0));
+    if (L > 0) {
+        if (k) CPD_CUDA(cudaMemcpy(k, s->trk.p, sizeof(int64_t) * L, cudaMemcpyDeviceToHost));
+        if (off_bound) CPD_CUDA(cudaMemcpy(off_bound, s->troff.p, sizeof(int64_t) * L, cudaMemcpyDeviceToHost));
+        if (rp) CPD_CUDA(cudaMemcpy(rp, s->trrp.p, sizeof(double) * L, cudaMemcpyDeviceToHost));
+    }
+    *len = h.traj_len;
+    ABI_END
+}
+
+int cpd_power_sigma(const cpd_problem* p, int32_t iters, uint64_t seed, double* sigma)
+{
+    ABI_BEGIN
+    if (!p || !sigma || iters < 1) return fail(CPD_E_ARG, "bad argument");
+    CPD_CUDA(cudaSetDevice(p->device));
+    Ctx cx(p);
+    DBuf<double> v(p->n), w(p->m);
+    *sigma = power_sigma(cx, iters, seed, 1.0, v.p, w.p);
+    ABI_END
+}
+
+int cpd_problem_score(const cpd_problem* p, const double* x, const double* y, int32_t mem, double out[8])
+{
+    ABI_BEGIN
+    if (!p || !x || !y || !out) return fail(CPD_E_ARG, "NULL argument");
+    CPD_CUDA(cudaSetDevice(p->device));
+    Ctx cx(p);
+    DBuf<double> dx, dy;
+    const double *px = x, *py = y;
+    if (mem != CPD_DEVICE) {
+        dx.alloc(p->n);
+        dy.alloc(p->m);
+        CPD_CUDA(cudaMemcpy(dx.p, x, sizeof(double) * p->n, cudaMemcpyHostToDevice));
+        CPD_CUDA(cudaMemcpy(dy.p, y, sizeof(double) * p->m, cudaMemcpyHostToDevice));
+        px = dx.p;
+        py = dy.p;
+    }
+    double nb, nc;
+    eval_norms(cx, p->b.p, p->c.p, &nb, &nc);
+    eval_score(cx, px, py, p->c.p, p->bounds(), nb, nc, out);
+    ABI_END
+}
+
+int cpd_compute_stats(const cpd_problem* p, const double* x, const double* z, const double* lhat,
+                      const double* uhat, double eps_abs, int64_t candidate_floor, int32_t mem,
+                      cpd_stats* out)
+{
+    ABI_BEGIN
+    if (!p || !x || !out || ((lhat == nullptr) != (uhat == nullptr))) return fail(CPD_E_ARG, "bad argument");
+    CPD_CUDA(cudaSetDevice(p->device));
+    Ctx cx(p);
+    DBuf<double> b[4];
+    const double* src[4] = {x, z, lhat, uhat};
+    const double* dev[4] = {x, z, lhat, uhat};
+    if (mem != CPD_DEVICE)
+        for (int i = 0; i < 4; ++i)
+            if (src[i]) {
+                b[i].alloc(p->n);
+                CPD_CUDA(cudaMemcpy(b[i].p, src[i], sizeof(double) * p->n, cudaMemcpyHostToDevice));
+                dev[i] = b[i].p;
+            }
+    eval_stats(cx, dev[0], dev[1], dev[2], dev[3], eps_abs, candidate_floor, 0, 0, out);
+    ABI_END
+}
+
+int cpd_get_kernel_times(cpd_solver* s, const char** names, double* ms, int64_t* launches, int32_t cap,
+                         int32_t* len, int32_t reset)
+{
+    ABI_BEGIN
+    if (!s || !len) return fail(CPD_E_ARG, "NULL argument");
+    int32_t L = 0;
+    for (int kind = 0; kind < 2; ++kind)
+        for (int k = 0; k < KT_N; ++k) {
+            if (L < cap) {
+                if (names) names[L] = KT_NAMES[kind][k];
+                if (ms) ms[L] = s->kt_ms[kind][k];
+                if (launches) launches[L] = s->kt_n[kind][k];
+            }
+            ++L;
+        }
+    *len = std::min(L, std::max(cap, 0));
+    if (reset) {
+        std::memset(s->kt_ms, 0, sizeof(s->kt_ms));
+        std::memset(s->kt_n, 0, sizeof(s->kt_n));
+    }
+    ABI_END
+}
+
+int cpd_kernel_bytes(const cpd_solver* s, const char* name, double* bytes)
+{
+    ABI_BEGIN
+    if (!s || !name || !bytes) return fail(CPD_E_ARG, "NULL argument");
+    *bytes = s->kernel_bytes(name);
+    if (*bytes < 0) return fail(CPD_E_ARG, std::string("unknown kernel ") + name);
+    ABI_END
+}
+
+}  // extern "C"
