@@ -196,6 +196,10 @@ int cpd_compute_stats(const cpd_problem *p, const double *x, const double *z,
  * of length *len (<= cap); names point to static strings.  Reset with reset=1. */
 int cpd_get_kernel_times(cpd_solver *s, const char **names, double *ms, int64_t *launches,
                          int32_t cap, int32_t *len, int32_t reset);
+/* Launch accounting of a solver: out = {kernels of this library launched on the
+ * solver's stream so far (every node of a graph launch counted), CUDA-graph
+ * launches, kernels per phase-1 batch graph, kernels per corner batch graph}. */
+int cpd_solver_counters(const cpd_solver *s, int64_t out[4]);
 /* Algorithmic bytes one launch of kernel `name` moves (DESIGN.md byte model). */
 int cpd_kernel_bytes(const cpd_solver *s, const char *name, double *bytes);
 

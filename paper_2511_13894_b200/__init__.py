@@ -30,7 +30,7 @@ DECLARED_SYMBOLS = [
     "cpd_params_default", "cpd_corner_params_default", "cpd_solver_create", "cpd_solver_destroy",
     "cpd_solve", "cpd_corner_push", "cpd_step", "cpd_get_iterate", "cpd_set_iterate", "cpd_get_stats",
     "cpd_get_trajectory", "cpd_power_sigma", "cpd_problem_score", "cpd_compute_stats",
-    "cpd_get_kernel_times", "cpd_kernel_bytes",
+    "cpd_get_kernel_times", "cpd_kernel_bytes", "cpd_solver_counters",
 ]
 
 
@@ -109,6 +109,7 @@ def lib():
             "cpd_compute_stats": (C.c_int, [P, P, P, P, P, D, I64, I32, C.POINTER(Stats)]),
             "cpd_get_kernel_times": (C.c_int, [P, P, P, P, I32, C.POINTER(I32), I32]),
             "cpd_kernel_bytes": (C.c_int, [P, C.c_char_p, C.POINTER(D)]),
+            "cpd_solver_counters": (C.c_int, [P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -322,6 +323,12 @@ class Solver:
         b = C.c_double()
         _check(lib().cpd_kernel_bytes(self.h, name.encode(), C.byref(b)))
         return b.value
+
+    def counters(self):
+        out = (C.c_int64 * 4)()
+        _check(lib().cpd_solver_counters(self.h, out))
+        return dict(zip(("launches", "graph_launches", "graph_kernels_phase1", "graph_kernels_corner"),
+                        list(out)))
 
     def close(self):
         if getattr(self, "h", None):

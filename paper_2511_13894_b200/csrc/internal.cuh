@@ -112,6 +112,7 @@ struct Ctx {
     DBuf<int32_t> lcntA, lcntAT;
     DBuf<double> lpartA, laccA, lpartAT, laccAT;
     int grid_elem = 0;
+    int64_t launches = 0;            // kernels of this library launched on `st` (graph nodes included)
     explicit Ctx(const cpd_problem* p);
     ~Ctx();
     DevPlan planA() const;

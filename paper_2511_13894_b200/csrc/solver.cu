@@ -90,12 +90,14 @@ void Ctx::set_i64(int64_t* f, int64_t v)
 {
     k_set_i64<<<1, 1, 0, st>>>(f, v);
     CPD_CUDA(cudaGetLastError());
+    ++launches;
 }
 
 void Ctx::set_i32(int32_t* f, int32_t v)
 {
     k_set_i32<<<1, 1, 0, st>>>(f, v);
     CPD_CUDA(cudaGetLastError());
+    ++launches;
 }
 
 void Ctx::sync() { CPD_CUDA(cudaStreamSynchronize(st)); }
@@ -120,6 +122,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
     const int gr = std::max(1, std::min(grid, dp.nent));
     k_spmv<NV, Epi><<<gr, TPB, 0, cx.st>>>(M.dev(), dp, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p);
     CPD_CUDA(cudaGetLastError());
+    ++cx.launches;
 }
 
 template <class Op>
@@ -129,6 +132,7 @@ void launch_elem(Ctx& cx, int64_t N, const Op& op, Gate g)
     const int gr = (int)std::max<int64_t>(1, std::min<int64_t>(need, cx.grid_elem));
     k_elem<Op><<<gr, TPB, 0, cx.st>>>(N, op, g, cx.ctl, cx.bpart.p, cx.ctr.p);
     CPD_CUDA(cudaGetLastError());
+    ++cx.launches;
 }
 
 static Gate always() { return Gate{GATE_ALWAYS, 0, 0, nullptr}; }
@@ -293,6 +297,8 @@ struct cpd_solver {
     int64_t kt_n[2][KT_N] = {};
     int nnodes = 0;
     const int64_t traj_cap = 1 << 16;
+    int64_t graph_kernels[2] = {0, 0};
+    int64_t graph_launches = 0;
 
     cpd_solver(const cpd_problem* p, const cpd_params& pr) : P(p), prm(pr), cx(p)
     {
@@ -394,6 +400,7 @@ struct cpd_solver {
     // ---------------------------------------------------------- one batch
     void enqueue_batch(int kind, bool capture)
     {
+        const int64_t l0 = cx.launches;
         const int32_t n = P->n, m = P->m;
         const int K = prm.check_every;
         const double* c = obj_of(kind);
@@ -439,6 +446,7 @@ struct cpd_solver {
                            Gate{GATE_K2, s, n2, active.p});
             rec(ev1, n2);
         }
+        if (capture) graph_kernels[kind] = cx.launches - l0;
         CPD_CUDA(cudaMemcpyAsync(h_active, active.p, sizeof(int32_t) * nnodes, cudaMemcpyDeviceToHost, cx.st));
         CPD_CUDA(cudaMemcpyAsync(cx.h_ctl, cx.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, cx.st));
     }
@@ -459,8 +467,11 @@ struct cpd_solver {
                 }
                 CPD_CUDA(cudaStreamEndCapture(cx.st, &graph[kind]));
                 CPD_CUDA(cudaGraphInstantiate(&gexec[kind], graph[kind], 0));
+                cx.launches -= graph_kernels[kind];   // capture counted them; launches count below
             }
             CPD_CUDA(cudaGraphLaunch(gexec[kind], cx.st));
+            cx.launches += graph_kernels[kind];
+            graph_launches += 1;
         } else {
             enqueue_batch(kind, false);
         }
@@ -520,6 +531,7 @@ struct cpd_solver {
             k_copy<<<g, 256, 0, cx.st>>>(P->n, Xp(cur_par), (k & 1) ? Xa1.p : Xa0.p);
             k_copy<<<g, 256, 0, cx.st>>>(P->m, Y.p, Ya.p);
             CPD_CUDA(cudaGetLastError());
+            cx.launches += 2;
         }
         run_active = false;
     }
@@ -594,6 +606,7 @@ struct cpd_solver {
         // phase-1 solution (x*, y*): x* stays in X[cur_par]; y* saved in Ystar
         k_copy<<<g, 256, 0, cx.st>>>(m, Ystar.p, Y.p);
         CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
         const double* obj = nullptr;
         if (cp.obj) {
             CPD_CUDA(cudaMemcpyAsync(objd.p, cp.obj, sizeof(double) * n,
@@ -644,6 +657,7 @@ struct cpd_solver {
         // y, z returned are phase 1's
         k_copy<<<g, 256, 0, cx.st>>>(m, Y.p, Ystar.p);
         CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
         if (after)
             eval_stats(cx, Xp(cur_par), Z.p, lhat.p, uhat.p, cp.eps_abs, cp.candidate_floor, fix_lb, fix_ub,
                        after);
@@ -987,6 +1001,17 @@ int cpd_get_kernel_times(cpd_solver* s, const char** names, double* ms, int64_t*
         std::memset(s->kt_ms, 0, sizeof(s->kt_ms));
         std::memset(s->kt_n, 0, sizeof(s->kt_n));
     }
+    ABI_END
+}
+
+int cpd_solver_counters(const cpd_solver* s, int64_t out[4])
+{
+    ABI_BEGIN
+    if (!s || !out) return fail(CPD_E_ARG, "NULL argument");
+    out[0] = s->cx.launches;
+    out[1] = s->graph_launches;
+    out[2] = s->graph_kernels[0];
+    out[3] = s->graph_kernels[1];
     ABI_END
 }
 
