@@ -33,11 +33,12 @@ struct DBuf {
     size_t n = 0;
     DBuf() = default;
     explicit DBuf(size_t count) { alloc(count); }
+    // +64 bytes of padding: TMA bulk copies read 16-byte-aligned supersets of ranges.
     void alloc(size_t count)
     {
         free();
         n = count;
-        if (count) CPD_CUDA(cudaMalloc(&p, sizeof(T) * count));
+        if (count) CPD_CUDA(cudaMalloc(&p, sizeof(T) * count + 64));
     }
     void free()
     {
@@ -62,12 +63,15 @@ struct DBuf {
 // nnz-balanced SpMV plan of one CSR layout (immutable, shared by solvers).
 struct Plan {
     DBuf<PlanEntry> ent;
-    DBuf<int64_t> long_off;
+    DBuf<int32_t> long_row, long_ptr, long_ents;
     int32_t nent = 0, nlong = 0;
-    int64_t chunks = 0;
-    int64_t stream_entries = 0, long_entries = 0;
+    int64_t rows_entries = 0, single_entries = 0, long_pieces = 0;
+    int32_t nslab = 1;
 };
-void build_plan(int32_t rows, const std::vector<int32_t>& rowptr, Plan& plan);
+// rows x cols CSR with device column array d_col; long rows are cut into CAP pieces
+// at column-slab boundaries and their pieces ordered slab-major.
+void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rowptr, const int32_t* d_p,
+                const int32_t* d_col, Plan& plan);
 
 struct Matrix {
     DBuf<int32_t> p, j;
@@ -109,8 +113,7 @@ struct Ctx {
     Ctl* h_ctl = nullptr;
     DBuf<double> bpart;
     DBuf<unsigned> ctr;
-    DBuf<int32_t> lcntA, lcntAT;
-    DBuf<double> lpartA, laccA, lpartAT, laccAT;
+    DBuf<double> lpartA, lpartAT;     // long-row piece partials of each layout
     int grid_elem = 0;
     int64_t launches = 0;            // kernels of this library launched on `st` (graph nodes included)
     explicit Ctx(const cpd_problem* p);

@@ -27,26 +27,32 @@
 namespace cpd {
 
 constexpr int TPB = 256;       // threads per CTA of every hot kernel
-constexpr int CAP = 2048;      // nonzeros per plan entry (8 per thread)
-constexpr int RMAX = 512;      // rows per stream entry
+constexpr int CAP = 2048;      // nonzeros per plan entry (one TMA stage)
+constexpr int RMAX = 256;      // rows per rows-entry
+constexpr int SINGLE_MIN = 256;  // a row with more nonzeros gets an entry of its own (block reduce)
+constexpr int NSTAGE = 3;      // TMA pipeline depth (stages per CTA)
+constexpr int NVECMAX = 5;     // staged per-row vectors per entry
 constexpr int NSMAX = 12;      // max scalars an epilogue reduces
 
 enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2 };
 enum { ST_RUNNING = -1, ST_CONVERGED = 0, ST_ITER_LIMIT = 1, ST_TIME_LIMIT = 2, ST_FAIL = 3 };
 enum { GATE_ALWAYS = 0, GATE_K1 = 1, GATE_K2 = 2, GATE_CHECK = 3, GATE_RESTART = 4 };
 
-// Plan entry: stream entry {row0, row1, log2(threads per row), -1}
-//             long chunk  {row, chunk, -1, long_id}
-struct PlanEntry { int32_t a, b, c, d; };
+// Plan entry (16 B):
+//   rows entry  {r0, r1, p0, p1}: rows [r0, r1) whose nonzeros are [p0, p1) (<= CAP)
+//   long piece  {slot, -1 - long_id, q0, q1}: nonzeros [q0, q1) of a long row, all inside
+//               one column slab (SURVEY §7 "gather locality"); its GW warp partials go
+//               to lpart[(slot * GW + wg) * 2 + v] (slots of one row are contiguous)
+struct PlanEntry { int32_t a, b, p0, p1; };
 
 struct DevPlan {
     const PlanEntry* ent;
     int32_t nent;
     int32_t nlong;
-    const int64_t* long_off;   // [nlong] first chunk slot of each long row
-    int32_t* long_cnt;         // [nlong] arrival counters (reset by the last arriver)
-    double* long_part;         // [chunks * 2] chunk partial sums (NV <= 2)
-    double* long_acc;          // [nlong * NSMAX] epilogue scalars of long rows
+    const int32_t* long_row;   // [nlong] row index of each long row
+    const int32_t* long_ptr;   // [nlong + 1] piece slots of each long row (column order)
+    const int32_t* long_ents;  // unused (kept for layout stability)
+    double* lpart;             // [pieces * GW * 2] warp partial sums (NV <= 2)
 };
 
 struct DevCsr {
@@ -186,7 +192,7 @@ __device__ __forceinline__ void warp_sum(double (&v)[NS])
 }
 
 // Deterministic block reduction; result valid in thread 0.
-template <int NS>
+template <int NS, int NT = TPB>
 __device__ __forceinline__ void block_sum(double (&v)[NS], double (*sw)[NS])
 {
     warp_sum<NS>(v);
@@ -200,27 +206,29 @@ __device__ __forceinline__ void block_sum(double (&v)[NS], double (*sw)[NS])
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
             double t = 0.0;
-            for (int i = 0; i < TPB / 32; ++i) t += sw[i][s];
+            for (int i = 0; i < NT / 32; ++i) t += sw[i][s];
             v[s] = t;
         }
     }
 }
 
-// Block partials -> last-block-done grid combine -> fin(totals) in thread 0 of the
-// last block.  `extra` (nextra x NS) are extra per-item partials (long rows).
-template <int NS, class Fin>
-__device__ __forceinline__ void grid_finalize(double (&acc)[NS], double* bpart, unsigned* ctr,
-                                              const double* extra, int nextra, Fin fin)
+// Block partial of `acc` stored at bpart[(prev + blockIdx.x) * NS]; the last block
+// to arrive sums bpart[0 .. prev + gridDim.x) in index order (deterministic) and
+// runs fin(totals) in its thread 0.  `prev` = partials a preceding kernel left
+// (the rows kernel of a plan with long rows), or 0.
+template <int NS, int NT = TPB, class Fin>
+__device__ __forceinline__ void grid_finalize(double (&acc)[NS], double* bpart, unsigned* ctr, int prev,
+                                              Fin fin)
 {
-    __shared__ double sw[TPB / 32][NS];
+    __shared__ double sw[NT / 32][NS];
     __shared__ int s_last;
-    block_sum<NS>(acc, sw);
+    block_sum<NS, NT>(acc, sw);
     if (threadIdx.x == 0) {
 #pragma unroll
-        for (int s = 0; s < NS; ++s) bpart[(size_t)blockIdx.x * NS + s] = acc[s];
+        for (int s = 0; s < NS; ++s) bpart[(size_t)(prev + blockIdx.x) * NS + s] = acc[s];
         __threadfence();
-        unsigned prev = atomicAdd(ctr, 1u);
-        s_last = (prev == gridDim.x - 1);
+        unsigned old = atomicAdd(ctr, 1u);
+        s_last = (old == gridDim.x - 1);
     }
     __syncthreads();
     if (!s_last) return;
@@ -228,13 +236,11 @@ __device__ __forceinline__ void grid_finalize(double (&acc)[NS], double* bpart, 
     double tot[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) tot[s] = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += TPB)
+    const int nb = prev + (int)gridDim.x;
+    for (int b = threadIdx.x; b < nb; b += NT)
 #pragma unroll
         for (int s = 0; s < NS; ++s) tot[s] += __ldcg(&bpart[(size_t)b * NS + s]);
-    for (int l = threadIdx.x; l < nextra; l += TPB)
-#pragma unroll
-        for (int s = 0; s < NS; ++s) tot[s] += __ldcg(&extra[(size_t)l * NSMAX + s]);
-    block_sum<NS>(tot, sw);
+    block_sum<NS, NT>(tot, sw);
     if (threadIdx.x == 0) {
         fin(tot);
         *ctr = 0u;
@@ -242,118 +248,452 @@ __device__ __forceinline__ void grid_finalize(double (&acc)[NS], double* bpart, 
     }
 }
 
+// Block partial only (no combine): the finishing kernel combines it.
+template <int NS, int NT = TPB>
+__device__ __forceinline__ void block_partial(double (&acc)[NS], double* bpart)
+{
+    __shared__ double sw[NT / 32][NS];
+    block_sum<NS, NT>(acc, sw);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int s = 0; s < NS; ++s) bpart[(size_t)blockIdx.x * NS + s] = acc[s];
+}
+
+// ------------------------------------------------------------ TMA / mbarrier (sm_90+ PTX, used on sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`; the
+// streamed bytes are marked evict-first in L2 so they do not push out the gathered
+// vector (y, or the current column slab of x).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // ------------------------------------------------------------ SpMV + epilogue
-// Row sums s_v = sum_k M_rk * vec_v[col_k] (v < NV) for every row r of M, each
-// handed to epi.row(r, s, acc).  Stream entries stage the products of up to CAP
-// nonzeros in shared memory (coalesced loads of col/val, one gather each), then
-// 2^lg threads reduce each row; long rows (> CAP nonzeros) are split into CAP
-// chunks whose partials the last-arriving CTA sums in chunk order.
+// Shared-memory stage of one plan entry, filled by the TMA engine: row pointers,
+// column indices, values and up to NVEC per-row input vectors of the epilogue.
+// Every array is copied as its 16-byte-aligned superset; consumers index with the
+// element offset of the first wanted element (arrays are padded by >= 16 bytes).
+template <int NVEC>
+struct alignas(16) Stage {
+    double val[CAP + 2];
+    double vec[NVEC > 0 ? NVEC : 1][RMAX + 2];
+    int32_t col[CAP + 4];
+    int32_t rp[RMAX + 8];
+};
+
+constexpr int NCW = 16;                   // consumer warps per CTA of k_spmv (one CTA per SM)
+constexpr int TPB_SP = (NCW + 1) * 32;    // + one TMA producer warp
+constexpr int NGRP = 2;                   // long-row pieces rotate over NGRP groups of consumer warps
+constexpr int GW = NCW / NGRP;            // warps per group
+constexpr int WCHUNK = CAP / GW;          // nonzeros per warp share of a long-row piece (8 per lane)
+constexpr size_t SMEM_BUDGET = 220 * 1024;
+
+template <int NV, int NVEC>
+struct StageSet {
+    Stage<NVEC> st;
+    double prod2[NV > 1 ? CAP : 2];   // second products (NV = 2)
+};
+// as many stages as fit one CTA per SM (<= 16)
+constexpr size_t SEG_BYTES = (size_t)NCW * 3 * 2 * 32 * sizeof(double);   // per-warp segment scratch (NV <= 2)
+template <int NV, int NVEC>
+constexpr int nstage_of()
+{
+    return (int)((SMEM_BUDGET - SEG_BYTES) / sizeof(StageSet<NV, NVEC>)) > 16
+               ? 16
+               : (int)((SMEM_BUDGET - SEG_BYTES) / sizeof(StageSet<NV, NVEC>));
+}
+
+template <int NV, int NVEC>
+struct alignas(16) SpmvSmem {
+    static constexpr int NS_ = nstage_of<NV, NVEC>();
+    StageSet<NV, NVEC> ss[NS_];
+    double seg[NCW][3][NV * 32];   // per-warp head / tail / complete row partials
+    uint64_t full[NS_];    // TMA -> consumers
+    uint64_t empty[NS_];   // consumer warps -> producer
+    PlanEntry ent[NS_];
+};
+
+__device__ __forceinline__ uint32_t al_dn16(uint64_t b) { return (uint32_t)(b & ~15ull); }
+
+struct VSrc {
+    const double* p[NVECMAX];
+};
+
+__device__ __forceinline__ uint32_t span_bytes(uint64_t esz, int64_t lo, int64_t hi)
+{
+    if (hi <= lo) return 0u;
+    const uint64_t a0 = ((uint64_t)lo * esz) & ~15ull;
+    const uint64_t a1 = ((uint64_t)hi * esz + 15ull) & ~15ull;
+    return (uint32_t)(a1 - a0);
+}
+
+__device__ __forceinline__ void span_copy(void* dst, const void* base, uint64_t esz, int64_t lo, int64_t hi,
+                                          uint64_t* bar)
+{
+    if (hi <= lo) return;
+    const uint64_t a0 = ((uint64_t)lo * esz) & ~15ull;
+    const uint64_t a1 = ((uint64_t)hi * esz + 15ull) & ~15ull;
+    tma_load_1d(dst, (const char*)base + a0, (uint32_t)(a1 - a0), bar);
+}
+
+// Issue the bulk copies of entry E into stage `st` (one thread): expect_tx with
+// the byte total first, then the copies.
+template <int NVEC>
+__device__ __forceinline__ void stage_issue(const PlanEntry& E, Stage<NVEC>& st, uint64_t* bar, const DevCsr& M,
+                                            const VSrc& vs)
+{
+    const bool rows = E.b >= 0;
+    uint32_t bytes = span_bytes(4, E.p0, E.p1) + span_bytes(8, E.p0, E.p1);
+    if (rows) bytes += span_bytes(4, E.a, (int64_t)E.b + 1);
+    if (rows)
+#pragma unroll
+        for (int v = 0; v < NVEC; ++v)
+            if (vs.p[v]) bytes += span_bytes(8, E.a, E.b);
+    mbar_arrive_expect_tx(bar, bytes);
+    span_copy(st.col, M.j, 4, E.p0, E.p1, bar);
+    span_copy(st.val, M.x, 8, E.p0, E.p1, bar);
+    if (rows) span_copy(st.rp, M.p, 4, E.a, (int64_t)E.b + 1, bar);
+    if (rows)
+#pragma unroll
+        for (int v = 0; v < NVEC; ++v)
+            if (vs.p[v]) span_copy(st.vec[v], vs.p[v], 8, E.a, E.b, bar);
+}
+
+// One consumer warp's share of staged entry `s` (plan index ei).
+//  rows entry: the warp owns the rows whose first nonzero lies in its 1/NCW share of
+//    the entry's nonzeros; it gathers vec[col] for them (lane-strided, coalesced,
+//    4 loads in flight per lane), forms the products in place in shared memory,
+//    then lane = row: sums the row and applies the fused epilogue (all lanes busy).
+//  long-row piece: consecutive pieces rotate over NGRP groups of GW warps (16 loads
+//    in flight per lane); each warp of the group sums its WCHUNK nonzeros and lane 0
+//    writes the warp partial to lpart[(ei * GW + wg) * 2 + v] for k_finish.
+// Returns true if the warp already released the stage (arrived on empty[s]).
 template <int NV, class Epi>
-__global__ void __launch_bounds__(TPB)
+__device__ __forceinline__ bool consume_entry(SpmvSmem<NV, Epi::NVEC>& S, int s, int ei, const DevPlan& P,
+                                              const Epi& e, const double* __restrict__ v0,
+                                              const double* __restrict__ v1, double (&acc)[Epi::NS], int w,
+                                              int lane, int& gbase, int& lbase)
+{
+    constexpr int NVEC = Epi::NVEC;
+    constexpr int U = 8;
+    const PlanEntry E = S.ent[s];
+    Stage<NVEC>& st = S.ss[s].st;
+    const int32_t* col = st.col + (E.p0 & 3);
+    double* val = st.val + (E.p0 & 1);
+    double* val2 = S.ss[s].prod2;
+    const int cnt = E.p1 - E.p0;
+    if (E.b >= 0) {
+        // rows entry: 32-row chunks; chunk j of this entry belongs to warp (gbase + j) % NCW
+        const int nr = E.b - E.a;
+        const int32_t* rp = st.rp + (E.a & 3);
+        const int p0 = E.p0;
+        const int nch = (nr + 31) >> 5;
+        int j = (w - gbase) % NCW;
+        if (j < 0) j += NCW;
+        gbase += nch;
+        const double* vin[NVEC > 0 ? NVEC : 1];
+#pragma unroll
+        for (int v = 0; v < NVEC; ++v) vin[v] = st.vec[v] + (E.a & 1);
+        for (; j < nch; j += NCW) {
+            const int rb = j * 32, re = min(rb + 32, nr);
+            const int qa = rp[rb] - p0, qb = rp[re] - p0;
+            for (int q0 = qa; q0 < qb; q0 += 32 * U) {
+                int c[U];
+                double g[U], g2[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = q0 + lane + 32 * u;
+                    c[u] = q < qb ? col[q] : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    g[u] = c[u] >= 0 ? __ldg(&v0[c[u]]) : 0.0;
+                    if (NV > 1) g2[u] = c[u] >= 0 ? __ldg(&v1[c[u]]) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = q0 + lane + 32 * u;
+                    if (q < qb) {
+                        const double a = val[q];
+                        val[q] = a * g[u];
+                        if (NV > 1) val2[q] = a * g2[u];
+                    }
+                }
+            }
+            __syncwarp();
+            // balanced segmented row sums: lane L sums the contiguous span
+            // [qa + L k, qa + (L+1) k) of the chunk's products; a row inside one span
+            // is complete there (cv), a row crossing spans is its start lane's tail (tv)
+            // + the through lanes' tails + its end lane's head (hv) — fixed order.
+            double* hv = S.seg[w][0];
+            double* tv = S.seg[w][1];
+            double* cv = S.seg[w][2];
+            const int n = qb - qa, k = (n + 31) >> 5;
+            const int s0 = qa + lane * k, s1 = min(s0 + k, qb);
+            if (s0 < s1) {
+                int lo = rb, hi = re - 1;   // last row with start <= s0
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (rp[mid] - p0 <= s0) lo = mid; else hi = mid - 1;
+                }
+                int r = lo;
+                bool before = rp[r] - p0 < s0;
+                double a[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) a[v] = 0.0;
+                int q = s0;
+                while (true) {
+                    const int rend = rp[r + 1] - p0;
+                    const int stop = min(rend, s1);
+                    for (; q < stop; ++q) {
+                        a[0] += val[q];
+                        if (NV > 1) a[NV - 1] += val2[q];
+                    }
+                    if (rend > s1) {   // row continues into the next span
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) tv[v * 32 + lane] = a[v];
+                        break;
+                    }
+                    double* dst = before ? hv + lane : cv + (r - rb);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) dst[v * 32] = a[v];
+                    ++r;
+                    if (r >= re || q >= s1) break;
+                    before = false;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) a[v] = 0.0;
+                }
+            }
+            __syncwarp();
+            const int i = rb + lane;
+            if (i < re) {
+                const int a0 = rp[i] - p0, a1 = rp[i + 1] - p0;
+                double sm[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) sm[v] = 0.0;
+                if (a1 > a0) {
+                    const int La = (a0 - qa) / k, Lb = (a1 - 1 - qa) / k;
+                    if (La == Lb) {
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) sm[v] = cv[v * 32 + (i - rb)];
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) {
+                            double t = tv[v * 32 + La];
+                            for (int L = La + 1; L < Lb; ++L) t += tv[v * 32 + L];
+                            sm[v] = t + hv[v * 32 + Lb];
+                        }
+                    }
+                }
+                e.row(E.a + i, sm, vin, i, acc);
+            }
+            __syncwarp();
+        }
+    } else {
+        // long-row piece: group (lbase % NGRP) of GW warps, WCHUNK nonzeros per warp.
+        // col/val are copied to registers and the stage is released before the gathers.
+        const int grp = lbase % NGRP;
+        ++lbase;
+        if (w / GW != grp) return false;
+        const int wg = w % GW;
+        const int q0 = wg * WCHUNK;
+        int c[WCHUNK / 32];
+        double a[WCHUNK / 32];
+#pragma unroll
+        for (int u = 0; u < WCHUNK / 32; ++u) {
+            const int q = q0 + lane + 32 * u;
+            c[u] = q < cnt ? col[q] : -1;
+            a[u] = q < cnt ? val[q] : 0.0;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[s]);
+        double sm[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sm[v] = 0.0;
+        double g[WCHUNK / 32], g2[WCHUNK / 32];
+#pragma unroll
+        for (int u = 0; u < WCHUNK / 32; ++u) {
+            g[u] = c[u] >= 0 ? __ldg(&v0[c[u]]) : 0.0;
+            if (NV > 1) g2[u] = c[u] >= 0 ? __ldg(&v1[c[u]]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < WCHUNK / 32; ++u) {
+            sm[0] += a[u] * g[u];
+            if (NV > 1) sm[NV - 1] += a[u] * g2[u];
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sm[v] += __shfl_xor_sync(0xffffffffu, sm[v], o);
+        if (lane == 0)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) P.lpart[((size_t)E.a * GW + wg) * 2 + v] = sm[v];
+        return true;
+    }
+    return false;
+}
+
+// Row sums s_v = sum_k M_rk * vec_v[col_k] (v < NV) for every row r of M, each handed
+// to the fused epilogue.  One persistent, warp-specialised CTA per SM walks the plan
+// round-robin: a producer warp stages each entry with the TMA engine (col, val, row
+// pointers and the epilogue's per-row inputs) into a ring of NS_ stages guarded by
+// full/empty mbarriers, and NCW consumer warps each process their own share of every
+// staged entry with no CTA-wide barrier.  Long-row pieces leave per-warp partials
+// that k_finish completes.
+template <int NV, class Epi>
+__global__ void __launch_bounds__(TPB_SP, 1)
 k_spmv(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* bpart,
        unsigned* ctr)
 {
     constexpr int NS = Epi::NS;
-    __shared__ double s_prod[NV][CAP];
-    __shared__ int32_t s_rp[RMAX + 1];
-    __shared__ double s_w[TPB / 32][NV];
+    constexpr int NVEC = Epi::NVEC;
+    using Smem = SpmvSmem<NV, NVEC>;
+    constexpr int NST = Smem::NS_;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    auto& S = *reinterpret_cast<Smem*>(smem_raw);
     __shared__ int s_go;
-    if (threadIdx.x == 0) {
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
         s_go = gate_open(gate, ctl);
         if (s_go && gate.active && blockIdx.x == 0) gate.active[gate.node] = 1;
+        if (s_go) {
+#pragma unroll
+            for (int s = 0; s < NST; ++s) {
+                mbar_init(&S.full[s], 1);
+                mbar_init(&S.empty[s], NCW);
+            }
+            fence_mbar_init();
+        }
     }
     __syncthreads();
     if (!s_go) return;
-    const double* __restrict__ v0 = vs0.get(ctl);
-    const double* __restrict__ v1 = vs1.get(ctl);
     Epi e = epi;
     e.load(ctl);
     double acc[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-    const int tid = threadIdx.x;
-
-    for (int ei = blockIdx.x; ei < P.nent; ei += gridDim.x) {
-        const PlanEntry E = P.ent[ei];
-        if (E.c >= 0) {
-            // ---------------- stream entry: rows [r0, r1)
-            const int r0 = E.a, nr = E.b - E.a;
-            for (int q = tid; q <= nr; q += TPB) s_rp[q] = M.p[r0 + q];
-            __syncthreads();
-            const int p0 = s_rp[0];
-            const int cnt = s_rp[nr] - p0;
-#pragma unroll 4
-            for (int q = tid; q < cnt; q += TPB) {
-                const int col = __ldg(&M.j[p0 + q]);
-                const double a = __ldg(&M.x[p0 + q]);
-                s_prod[0][q] = a * __ldg(&v0[col]);
-                if (NV > 1) s_prod[NV - 1][q] = a * __ldg(&v1[col]);
-            }
-            __syncthreads();
-            const int lg = E.c, tpr = 1 << lg, lane = tid & (tpr - 1);
-            const int per_round = TPB >> lg;
-            for (int base = 0; base < nr; base += per_round) {
-                const int g = base + (tid >> lg);
-                double s[NV];
+    const int G = gridDim.x;
+    if (w == NCW) {
+        // ---------------- producer warp (one lane)
+        if (lane == 0) {
+            VSrc vsrc;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) s[v] = 0.0;
-                if (g < nr) {
-                    const int qa = s_rp[g] - p0, qb = s_rp[g + 1] - p0;
-                    for (int q = qa + lane; q < qb; q += tpr)
-#pragma unroll
-                        for (int v = 0; v < NV; ++v) s[v] += s_prod[v][q];
+            for (int v = 0; v < NVECMAX; ++v) vsrc.p[v] = v < NVEC ? e.vec(v) : nullptr;
+            uint32_t eph = 0;
+            int s = 0, it = 0;
+            for (int ei = blockIdx.x; ei < P.nent; ei += G, ++it) {
+                const PlanEntry E = P.ent[ei];
+                if (it >= NST) {
+                    mbar_wait(&S.empty[s], (eph >> s) & 1u);
+                    eph ^= 1u << s;
+                    fence_proxy_async_smem();
                 }
-                for (int o = tpr >> 1; o > 0; o >>= 1)
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
-                if (g < nr && lane == 0) e.row(r0 + g, s, acc);
+                S.ent[s] = E;
+                stage_issue<NVEC>(E, S.ss[s].st, &S.full[s], M, vsrc);
+                s = s + 1 == NST ? 0 : s + 1;
             }
-            __syncthreads();
-        } else {
-            // ---------------- long-row chunk
-            const int row = E.a, chunk = E.b, lid = E.d;
-            const int rp0 = M.p[row], rp1 = M.p[row + 1];
-            const int q0 = rp0 + chunk * CAP;
-            const int q1 = min(q0 + CAP, rp1);
-            double s[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) s[v] = 0.0;
-#pragma unroll 4
-            for (int q = q0 + tid; q < q1; q += TPB) {
-                const int col = __ldg(&M.j[q]);
-                const double a = __ldg(&M.x[q]);
-                s[0] += a * __ldg(&v0[col]);
-                if (NV > 1) s[NV - 1] += a * __ldg(&v1[col]);
-            }
-            block_sum<NV>(s, s_w);
-            if (tid == 0) {
-                const int64_t off = P.long_off[lid];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) P.long_part[(off + chunk) * 2 + v] = s[v];
-                __threadfence();
-                const int nch = (rp1 - rp0 + CAP - 1) / CAP;
-                const int prev = atomicAdd(&P.long_cnt[lid], 1);
-                if (prev == nch - 1) {
-                    __threadfence();
-                    double full[NV];
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) full[v] = 0.0;
-                    for (int c = 0; c < nch; ++c)
-#pragma unroll
-                        for (int v = 0; v < NV; ++v) full[v] += __ldcg(&P.long_part[(off + c) * 2 + v]);
-                    P.long_cnt[lid] = 0;
-                    double la[NS];
-#pragma unroll
-                    for (int s2 = 0; s2 < NS; ++s2) la[s2] = 0.0;
-                    e.row(row, full, la);
-#pragma unroll
-                    for (int s2 = 0; s2 < NS; ++s2) P.long_acc[(size_t)lid * NSMAX + s2] = la[s2];
-                }
-            }
-            __syncthreads();
+        }
+        __syncwarp();
+    } else {
+        // ---------------- consumer warps
+        const double* __restrict__ v0 = vs0.get(ctl);
+        const double* __restrict__ v1 = vs1.get(ctl);
+        uint32_t fph = 0;
+        int s = 0, gbase = 0, lbase = 0;
+        for (int ei = blockIdx.x; ei < P.nent; ei += G) {
+            mbar_wait(&S.full[s], (fph >> s) & 1u);
+            fph ^= 1u << s;
+            const bool released = consume_entry<NV, Epi>(S, s, ei, P, e, v0, v1, acc, w, lane, gbase, lbase);
+            __syncwarp();
+            if (lane == 0 && !released) mbar_arrive(&S.empty[s]);
+            s = s + 1 == NST ? 0 : s + 1;
         }
     }
-    grid_finalize<NS>(acc, bpart, ctr, P.long_acc, P.nlong, [&](double* tot) { e.finalize(tot, ctl); });
+    if (P.nlong == 0)
+        grid_finalize<NS, TPB_SP>(acc, bpart, ctr, 0, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+    else
+        block_partial<NS, TPB_SP>(acc, bpart);
+}
+
+// Long rows: one CTA per long row sums the row's contiguous warp partials (fixed
+// order: strided per thread, then the block tree), runs the epilogue on the full
+// row sum, then combines this kernel's block partials with those k_spmv left
+// (first `prev` slots) and finalizes.
+template <int NV, class Epi>
+__global__ void __launch_bounds__(TPB)
+k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, int prev)
+{
+    constexpr int NS = Epi::NS;
+    constexpr int NVEC = Epi::NVEC;
+    __shared__ int s_go;
+    __shared__ double s_w[TPB / 32][NV];
+    if (threadIdx.x == 0) s_go = gate_open(gate, ctl);
+    __syncthreads();
+    if (!s_go) return;
+    Epi e = epi;
+    e.load(ctl);
+    const double* vin[NVEC > 0 ? NVEC : 1];
+#pragma unroll
+    for (int v = 0; v < NVEC; ++v) vin[v] = e.vec(v);
+    double acc[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+    for (int l = blockIdx.x; l < P.nlong; l += gridDim.x) {
+        double sm[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sm[v] = 0.0;
+        const int64_t t0 = (int64_t)P.long_ptr[l] * GW, t1 = (int64_t)P.long_ptr[l + 1] * GW;
+        for (int64_t t = t0 + threadIdx.x; t < t1; t += TPB)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) sm[v] += __ldcg(&P.lpart[t * 2 + v]);
+        block_sum<NV>(sm, s_w);
+        if (threadIdx.x == 0) {
+            const int r = P.long_row[l];
+            e.row(r, sm, vin, r, acc);
+        }
+    }
+    grid_finalize<NS>(acc, bpart, ctr, prev, [e, ctl](double* tot) { e.finalize(tot, ctl); });
 }
 
 // Elementwise pass over [0, N) with reductions and a device-side finalize.
@@ -376,7 +716,7 @@ k_elem(int64_t N, Op op, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr)
     for (int s = 0; s < NS; ++s) acc[s] = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < N; i += (int64_t)gridDim.x * TPB)
         o.elem(i, acc);
-    grid_finalize<NS>(acc, bpart, ctr, nullptr, 0, [&](double* tot) { o.finalize(tot, ctl); });
+    grid_finalize<NS>(acc, bpart, ctr, 0, [o, ctl](double* tot) { o.finalize(tot, ctl); });
 }
 
 // ------------------------------------------------------------ epilogues
@@ -387,37 +727,50 @@ struct PingPong {
 };
 
 // a2 + a5 + n-side of a6, and the per-iteration termination decision F(k).
-struct EpiPrimal {
+// Staged per-row inputs: 0 c, 1 x_k, 2 x_avg, 3 lb, 4 ub (3-4 only with per-element
+// bounds, PE = true: the corner model, or an LP with non-uniform bounds).
+template <bool PE>
+struct EpiPrimalT {
     static constexpr int NS = 4;   // c^T x_k, ||r_D(y_k)||^2, bound terms, #nonfinite(x_{k+1})
+    static constexpr int NVEC = PE ? 5 : 3;
     const double* c;
     Bounds bd;
     PingPong X, Xa;
     // loaded
-    double tau, inv_t1;
+    double tau, inv_t;
     const double* xc;
     double* xn;
     const double* xac;
     double* xan;
-    double t1;
     __device__ void load(const Ctl* ctl)
     {
         tau = ctl->tau;
-        t1 = (double)(ctl->t + 1);
+        inv_t = 1.0 / (double)(ctl->t + 1);
         xc = X.at(ctl->k);
         xn = X.at(ctl->k + 1);
         xac = Xa.at(ctl->k);
         xan = Xa.at(ctl->k + 1);
     }
-    __device__ __forceinline__ void row(int j, const double* s, double* acc) const
+    __device__ __forceinline__ const double* vec(int v) const
     {
-        const double cj = c[j];
+        return v == 0 ? c : v == 1 ? xc : v == 2 ? xac : v == 3 ? bd.l : bd.u;
+    }
+    // row j of A^T; vin[v][li] = staged (or global, li = j) input v of row j
+    __device__ __forceinline__ void row(int j, const double* s, const double* const* vin, int li,
+                                        double* acc) const
+    {
+        const double cj = vin[0][li];
         const double z = cj - s[0];
-        const double x = xc[j];
-        const double lo = bd.lo(j), hi = bd.hi(j);
+        const double x = vin[1][li];
+        double lo = bd.l0, hi = bd.u0;
+        if constexpr (PE) {
+            lo = vin[3][li];
+            hi = vin[4][li];
+        }
         const double xp = proj(x - tau * z, lo, hi);
         xn[j] = xp;
-        const double xa = xac[j];
-        xan[j] = xa + (xp - xa) / t1;
+        const double xa = vin[2][li];
+        xan[j] = xa + (xp - xa) * inv_t;   // (x+ - x_avg)/t as a multiply (<= 1 ulp)
         acc[0] += cj * x;
         dual_terms(z, lo, hi, acc[1], acc[2]);
         acc[3] += isfinite(xp) ? 0.0 : 1.0;
@@ -443,27 +796,36 @@ struct EpiPrimal {
     }
 };
 
+using EpiPrimal = EpiPrimalT<true>;
+
 // a3 + a4 + a5 + m-side of a6: y+ = y + sigma (b - (2 A x+ - A x)).
+// Staged per-row inputs: 0 b, 1 y_k, 2 (A x_k), 3 y_avg.
 struct EpiDual {
     static constexpr int NS = 3;   // ||b - A x_{k+1}||^2, b^T y_{k+1}, #nonfinite(y_{k+1})
+    static constexpr int NVEC = 4;
     const double* b;
     double *y, *ya, *ax;
-    double sigma, t1;
+    double sigma, inv_t;
     __device__ void load(const Ctl* ctl)
     {
         sigma = ctl->sigma;
-        t1 = (double)(ctl->t + 1);
+        inv_t = 1.0 / (double)(ctl->t + 1);
     }
-    __device__ __forceinline__ void row(int i, const double* s, double* acc) const
+    __device__ __forceinline__ const double* vec(int v) const
+    {
+        return v == 0 ? b : v == 1 ? y : v == 2 ? ax : ya;
+    }
+    __device__ __forceinline__ void row(int i, const double* s, const double* const* vin, int li,
+                                        double* acc) const
     {
         const double axn = s[0];
-        const double bi = b[i];
-        const double yo = y[i];
-        const double yp = yo + sigma * (bi - (2.0 * axn - ax[i]));
+        const double bi = vin[0][li];
+        const double yo = vin[1][li];
+        const double yp = yo + sigma * (bi - (2.0 * axn - vin[2][li]));
         y[i] = yp;
         ax[i] = axn;
-        const double yav = ya[i];
-        ya[i] = yav + (yp - yav) / t1;
+        const double yav = vin[3][li];
+        ya[i] = yav + (yp - yav) * inv_t;
         const double r = bi - axn;
         acc[0] += r * r;
         acc[1] += bi * yp;
@@ -487,6 +849,8 @@ struct EpiDual {
 // a7, A^T pass of a check: (A^T y_k), (A^T y_avg) -> current & average n-side terms.
 struct EpiCheckN {
     static constexpr int NS = 9;   // ctx_c, rd2_c, bnd_c, dx2_c, ctx_a, rd2_a, bnd_a, dx2_a, off_bound(x_k; M)
+    static constexpr int NVEC = 0;
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     const double* c;
     Bounds bd;       // bounds of the run's model
     Bounds orig;     // original bounds (trajectory count)
@@ -503,7 +867,7 @@ struct EpiCheckN {
         traj = ctl->traj_on;
         eps_abs = ctl->eps_abs;
     }
-    __device__ __forceinline__ void row(int j, const double* s, double* acc) const
+    __device__ __forceinline__ void row(int j, const double* s, const double* const*, int, double* acc) const
     {
         const double cj = c[j];
         const double lo = bd.lo(j), hi = bd.hi(j);
@@ -530,10 +894,12 @@ struct EpiCheckN {
 // then the check decision (termination of current / average, restart, omega).
 struct EpiCheckM {
     static constexpr int NS = 4;   // rp2_a, bty_a, dy2_c, dy2_a
+    static constexpr int NVEC = 0;
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     const double *b, *y, *ya, *yr;
     double* axa;
     __device__ void load(const Ctl*) {}
-    __device__ __forceinline__ void row(int i, const double* s, double* acc) const
+    __device__ __forceinline__ void row(int i, const double* s, const double* const*, int, double* acc) const
     {
         axa[i] = s[0];
         const double bi = b[i];
@@ -694,10 +1060,12 @@ struct OpNorms {
 // Run-start evaluation: A x_0 -> Ax buffer, ||b - A x_0||^2, b^T y_0.
 struct EpiInitM {
     static constexpr int NS = 2;
+    static constexpr int NVEC = 0;
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     const double *b, *y;
     double* ax;   // may be null (score only)
     __device__ void load(const Ctl*) {}
-    __device__ __forceinline__ void row(int i, const double* s, double* acc) const
+    __device__ __forceinline__ void row(int i, const double* s, const double* const*, int, double* acc) const
     {
         if (ax) ax[i] = s[0];
         const double r = b[i] - s[0];
@@ -714,11 +1082,13 @@ struct EpiInitM {
 // Run-start evaluation: A^T y_0 -> S_r = score(x_0, y_0); FULL: converged at k = 0?
 struct EpiInitN {
     static constexpr int NS = 3;
+    static constexpr int NVEC = 0;
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     const double *c, *x;
     Bounds bd;
     int decide;   // 0: only store the score in ctl->last
     __device__ void load(const Ctl*) {}
-    __device__ __forceinline__ void row(int j, const double* s, double* acc) const
+    __device__ __forceinline__ void row(int j, const double* s, const double* const*, int, double* acc) const
     {
         const double cj = c[j];
         acc[0] += cj * x[j];
@@ -758,17 +1128,21 @@ struct OpPowInit {
 };
 struct EpiPowM {
     static constexpr int NS = 1;
+    static constexpr int NVEC = 0;
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     double* w;
     double inv;
     __device__ void load(const Ctl* ctl) { inv = ctl->pw_inv; }
-    __device__ __forceinline__ void row(int i, const double* s, double*) const { w[i] = s[0] * inv; }
+    __device__ __forceinline__ void row(int i, const double* s, const double* const*, int, double*) const { w[i] = s[0] * inv; }
     __device__ void finalize(const double*, Ctl*) const {}
 };
 struct EpiPowN {
     static constexpr int NS = 1;
+    static constexpr int NVEC = 0;
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     double* v;
     __device__ void load(const Ctl*) {}
-    __device__ __forceinline__ void row(int j, const double* s, double* acc) const
+    __device__ __forceinline__ void row(int j, const double* s, const double* const*, int, double* acc) const
     {
         v[j] = s[0];
         acc[0] += s[0] * s[0];
@@ -786,6 +1160,8 @@ struct EpiPowN {
 // a8: z = c - A^T y*, Algorithm 1 bound map, Uniform objective.
 struct EpiCorner {
     static constexpr int NS = 2;   // fix_lb, fix_ub
+    static constexpr int NVEC = 0;
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     const double *c, *x;
     Bounds bd;
     double *z, *lhat, *uhat, *chat;
@@ -793,7 +1169,7 @@ struct EpiCorner {
     double eps_abs, obj_scale;
     uint64_t seed;
     __device__ void load(const Ctl*) {}
-    __device__ __forceinline__ void row(int j, const double* s, double* acc) const
+    __device__ __forceinline__ void row(int j, const double* s, const double* const*, int, double* acc) const
     {
         const double zj = c[j] - s[0];
         z[j] = zj;

@@ -15,36 +15,53 @@
 namespace cpd {
 
 // ------------------------------------------------------------------ plans
-// Stream entries: consecutive rows with <= CAP nonzeros and <= RMAX rows; rows
-// longer than CAP become ceil(len/CAP) long-row chunks.  Threads per row in a
-// stream entry: smallest power of two with ~<= 4 nonzeros per thread (<= 32).
-void build_plan(int32_t rows, const std::vector<int32_t>& rp, Plan& plan)
+// Column slab width for long-row pieces: 4M columns = 32 MB of the gathered fp64
+// vector, so the slab being swept stays resident in the 126 MB L2.
+constexpr int64_t SLAB_COLS = 4 << 20;
+
+// pos[l * nb + s - 1] = first position q of long row l with col[q] >= s * SLAB_COLS.
+__global__ void k_slab_pos(int32_t nl, int32_t nb, const int32_t* lrows, const int32_t* p,
+                           const int32_t* col, int32_t* pos)
+{
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (int64_t)nl * nb;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t l = (int32_t)(idx / nb);
+        const int64_t target = (idx % nb + 1) * SLAB_COLS;
+        const int32_t r = lrows[l];
+        int32_t lo = p[r], hi = p[r + 1];
+        while (lo < hi) {
+            const int32_t mid = lo + (hi - lo) / 2;
+            if ((int64_t)col[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        pos[idx] = lo;
+    }
+}
+
+// Rows entries: maximal runs of consecutive rows with <= CAP nonzeros and <= RMAX
+// rows.  A row with more than SINGLE_MIN nonzeros is LONG: cut at column-slab
+// boundaries and into CAP pieces, pieces ordered slab-major after all rows entries
+// (while the CTAs sweep one slab, that slab of the gathered vector stays in L2);
+// k_finish sums its pieces and applies its epilogue.
+void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, const int32_t* d_p,
+                const int32_t* d_col, Plan& plan)
 {
     std::vector<PlanEntry> ent;
-    std::vector<int64_t> loff;
-    int64_t chunks = 0, nstream = 0, nlongent = 0;
+    std::vector<int32_t> lrows;
+    int64_t nrows_e = 0, nsingle = 0;
     int32_t r0 = 0;
     int64_t cur = 0;
     auto flush = [&](int32_t r1) {
         if (r1 > r0) {
-            const int nr = r1 - r0;
-            const double avg = (double)cur / nr;
-            int lg = 0;
-            while (lg < 5 && (double)(1 << lg) * 4.0 < avg) ++lg;
-            ent.push_back(PlanEntry{r0, r1, lg, -1});
-            ++nstream;
+            ent.push_back(PlanEntry{r0, r1, rp[r0], rp[r1]});
+            ++nrows_e;
         }
     };
     for (int32_t r = 0; r < rows; ++r) {
         const int64_t len = (int64_t)rp[r + 1] - rp[r];
-        if (len > CAP) {
+        if (len > SINGLE_MIN) {
+            // long row: pieces (any length > SINGLE_MIN; k_finish applies its epilogue)
             flush(r);
-            const int32_t nch = (int32_t)((len + CAP - 1) / CAP);
-            const int32_t lid = (int32_t)loff.size();
-            loff.push_back(chunks);
-            chunks += nch;
-            for (int32_t c = 0; c < nch; ++c) ent.push_back(PlanEntry{r, c, -1, lid});
-            nlongent += nch;
+            lrows.push_back(r);
             r0 = r + 1;
             cur = 0;
             continue;
@@ -57,18 +74,60 @@ void build_plan(int32_t rows, const std::vector<int32_t>& rp, Plan& plan)
         cur += len;
     }
     flush(rows);
-    if (ent.size() > (size_t)INT32_MAX) throw Error(CPD_E_DIM, "plan too large");
+    // long rows: slab boundaries (device binary search), pieces
+    const int32_t nl = (int32_t)lrows.size();
+    const int32_t nslab = (int32_t)std::max<int64_t>(1, ((int64_t)cols + SLAB_COLS - 1) / SLAB_COLS);
+    const int32_t nb = nslab - 1;
+    std::vector<int32_t> pos((size_t)nl * std::max(nb, 0));
+    if (nl > 0 && nb > 0) {
+        DBuf<int32_t> dl(nl), dpos((size_t)nl * nb);
+        CPD_CUDA(cudaMemcpy(dl.p, lrows.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice));
+        const int64_t tot = (int64_t)nl * nb;
+        k_slab_pos<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256>>>(nl, nb, dl.p, d_p, d_col, dpos.p);
+        CPD_CUDA(cudaGetLastError());
+        CPD_CUDA(cudaMemcpy(pos.data(), dpos.p, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost));
+    }
+    // pieces[s] = list of (long id, q0, q1) in row order
+    std::vector<std::vector<PlanEntry>> by_slab(nslab);
+    std::vector<std::vector<int32_t>> row_pieces_slab(nl);   // (slab, piece) order per row
+    for (int32_t l = 0; l < nl; ++l) {
+        const int32_t r = lrows[l];
+        int32_t a = rp[r];
+        for (int32_t s = 0; s < nslab; ++s) {
+            const int32_t b = (s + 1 < nslab) ? pos[(size_t)l * nb + s] : rp[r + 1];
+            for (int32_t q = a; q < b; q += CAP)
+                by_slab[s].push_back(PlanEntry{r, -1 - l, q, std::min(q + CAP, b)});
+            a = b;
+        }
+    }
+    // slots: the pieces of long row l occupy [lptr[l], lptr[l+1]) in column order
+    std::vector<int32_t> lptr(nl + 1, 0);
+    for (int32_t s = 0; s < nslab; ++s)
+        for (const PlanEntry& E : by_slab[s]) lptr[-1 - E.b + 1]++;
+    for (int32_t l = 0; l < nl; ++l) lptr[l + 1] += lptr[l];
+    std::vector<int32_t> next(lptr.begin(), lptr.end() - 1), lents;
+    int64_t npieces = 0;
+    for (int32_t s = 0; s < nslab; ++s)
+        for (PlanEntry E : by_slab[s]) {
+            E.a = next[-1 - E.b]++;   // slab-major visit == column order within each row
+            ent.push_back(E);
+            ++npieces;
+        }
+    if (ent.size() > (size_t)INT32_MAX / 2) throw Error(CPD_E_DIM, "plan too large");
     plan.nent = (int32_t)ent.size();
-    plan.nlong = (int32_t)loff.size();
-    plan.chunks = chunks;
-    plan.stream_entries = nstream;
-    plan.long_entries = nlongent;
+    plan.nlong = nl;
+    plan.rows_entries = nrows_e;
+    plan.single_entries = nsingle;
+    plan.long_pieces = npieces;
+    (void)lents;
+    plan.nslab = nslab;
     plan.ent.alloc(std::max<size_t>(ent.size(), 1));
     CPD_CUDA(cudaMemcpy(plan.ent.p, ent.data(), sizeof(PlanEntry) * ent.size(), cudaMemcpyHostToDevice));
-    plan.long_off.alloc(std::max<size_t>(loff.size(), 1));
-    if (!loff.empty())
-        CPD_CUDA(cudaMemcpy(plan.long_off.p, loff.data(), sizeof(int64_t) * loff.size(),
-                            cudaMemcpyHostToDevice));
+    plan.long_row.alloc(std::max(nl, 1));
+    plan.long_ptr.alloc(nl + 1);
+    plan.long_ents.alloc(1);
+    if (nl) CPD_CUDA(cudaMemcpy(plan.long_row.p, lrows.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice));
+    CPD_CUDA(cudaMemcpy(plan.long_ptr.p, lptr.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice));
 }
 
 // ------------------------------------------------------------ validation
@@ -356,8 +415,8 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         std::vector<int32_t> hp((size_t)m + 1), htp((size_t)n + 1);
         CPD_CUDA(cudaMemcpy(hp.data(), P->A.p.p, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
         CPD_CUDA(cudaMemcpy(htp.data(), P->AT.p.p, sizeof(int32_t) * htp.size(), cudaMemcpyDeviceToHost));
-        build_plan(m, hp, P->A.plan);
-        build_plan(n, htp, P->AT.plan);
+        build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.plan);
+        build_plan(n, m, htp, P->AT.p.p, P->AT.j.p, P->AT.plan);
         CPD_CUDA(cudaDeviceSynchronize());
     } catch (...) {
         delete P;

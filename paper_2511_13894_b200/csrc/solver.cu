@@ -35,19 +35,13 @@ Ctx::Ctx(const cpd_problem* p) : P(p)
     std::memset(h_aux, 0, sizeof(Ctl));
     ctl = ctl_main.p;
     h_ctl = h_main;
-    bpart.alloc((size_t)p->num_sms * 8 * NSMAX);
+    bpart.alloc((size_t)p->num_sms * 16 * NSMAX);
     ctr.alloc(1);
     CPD_CUDA(cudaMemset(ctr.p, 0, sizeof(unsigned)));
     const Plan& pa = p->A.plan;
     const Plan& pt = p->AT.plan;
-    lcntA.alloc(std::max(1, pa.nlong));
-    lcntAT.alloc(std::max(1, pt.nlong));
-    CPD_CUDA(cudaMemset(lcntA.p, 0, sizeof(int32_t) * lcntA.n));
-    CPD_CUDA(cudaMemset(lcntAT.p, 0, sizeof(int32_t) * lcntAT.n));
-    lpartA.alloc(std::max<int64_t>(1, pa.chunks * 2));
-    lpartAT.alloc(std::max<int64_t>(1, pt.chunks * 2));
-    laccA.alloc((size_t)std::max(1, pa.nlong) * NSMAX);
-    laccAT.alloc((size_t)std::max(1, pt.nlong) * NSMAX);
+    lpartA.alloc((size_t)std::max<int64_t>(1, pa.long_pieces) * GW * 2);
+    lpartAT.alloc((size_t)std::max<int64_t>(1, pt.long_pieces) * GW * 2);
     grid_elem = p->num_sms * 4;
 }
 
@@ -61,13 +55,13 @@ Ctx::~Ctx()
 DevPlan Ctx::planA() const
 {
     const Plan& pl = P->A.plan;
-    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.long_off.p, lcntA.p, lpartA.p, laccA.p};
+    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p, lpartA.p};
 }
 
 DevPlan Ctx::planAT() const
 {
     const Plan& pl = P->AT.plan;
-    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.long_off.p, lcntAT.p, lpartAT.p, laccAT.p};
+    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p, lpartAT.p};
 }
 
 void Ctx::pull_ctl()
@@ -108,21 +102,32 @@ template <int NV, class Epi>
 void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel v1, const Epi& epi,
                  Gate g)
 {
+    constexpr size_t SMEM = sizeof(SpmvSmem<NV, Epi::NVEC>);
     static int grid = 0, sms = 0;
     {
         std::lock_guard<std::mutex> lk(g_grid_mu);
         if (!grid || sms != cx.P->num_sms) {
+            CPD_CUDA(cudaFuncSetAttribute(k_spmv<NV, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)SMEM));
             int nb = 0;
-            CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spmv<NV, Epi>, TPB, 0));
+            CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spmv<NV, Epi>, TPB_SP, SMEM));
             nb = std::max(1, std::min(nb, 8));
             sms = cx.P->num_sms;
             grid = nb * sms;
         }
     }
     const int gr = std::max(1, std::min(grid, dp.nent));
-    k_spmv<NV, Epi><<<gr, TPB, 0, cx.st>>>(M.dev(), dp, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p);
+    k_spmv<NV, Epi><<<gr, TPB_SP, SMEM, cx.st>>>(M.dev(), dp, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p);
     CPD_CUDA(cudaGetLastError());
     ++cx.launches;
+    if (dp.nlong > 0) {
+        const int gf = std::max(1, std::min(cx.P->num_sms * 8, dp.nlong));
+        Gate g2 = g;
+        g2.active = nullptr;
+        k_finish<NV, Epi><<<gf, TPB, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, gr);
+        CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
+    }
 }
 
 template <class Op>
@@ -240,10 +245,15 @@ __global__ void k_zero(int64_t N, double* dst)
 // z = c - A^T y
 struct EpiZ {
     static constexpr int NS = 1;
+    static constexpr int NVEC = 0;
     const double* c;
     double* z;
     __device__ void load(const Ctl*) {}
-    __device__ __forceinline__ void row(int j, const double* s, double*) const { z[j] = c[j] - s[0]; }
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
+    __device__ __forceinline__ void row(int j, const double* s, const double* const*, int, double*) const
+    {
+        z[j] = c[j] - s[0];
+    }
     __device__ void finalize(const double*, Ctl*) const {}
 };
 
@@ -436,9 +446,14 @@ struct cpd_solver {
         }
         for (int s = 0; s < K; ++s) {
             const int n1 = NODE_K0 + 2 * s, n2 = n1 + 1;
-            EpiPrimal e1{c, bd, X, Xa, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr, 0.0};
             rec(ev0, n1);
-            launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), e1, Gate{GATE_K1, s, n1, active.p});
+            if (kind == 0 && P->uniform_bounds) {   // scalar bounds: 3 staged per-row inputs
+                EpiPrimalT<false> e1{c, bd, X, Xa, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+                launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), e1, Gate{GATE_K1, s, n1, active.p});
+            } else {
+                EpiPrimalT<true> e1{c, bd, X, Xa, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+                launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), e1, Gate{GATE_K1, s, n1, active.p});
+            }
             rec(ev1, n1);
             EpiDual e2{P->b.p, Y.p, Ya.p, AX.p, 0.0, 0.0};
             rec(ev0, n2);
