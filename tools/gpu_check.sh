@@ -1,0 +1,20 @@
+#!/bin/bash
+# One GPU session: build, gpu tests, bench, ncu launch list + full capture of K1/K2.
+# Usage (from the repo root on the GPU box): bash tools/gpu_check.sh [tag]
+TAG=${1:-run}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/smi.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo BUILD FAILED; tail -30 $OUT/build.log; exit 1; }
+timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+tail -3 $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+tail -2 $OUT/smoke.log
+timeout 1500 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
+tail -c 3000 $OUT/bench.json
+if [ "${NCU:-1}" = "1" ]; then
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --tte '' > $OUT/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+  timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:EpiPrimal|EpiDual" -s 3 -c 6 \
+     -o $OUT/full python tools/prof_run.py --iters 4 > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
+fi
