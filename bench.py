@@ -223,10 +223,10 @@ def time_to_eps(names, device):
         S.solve()   # warm-up (graph capture)
         S.set_iterate(None, None)
         r = S.solve()
-        S.set_iterate(None, None)
-        rc, _, _ = S.corner_push(max_iters=200000)
+        rc, _, _ = S.corner_push(max_iters=200000)   # Algorithm 1 from the phase-1 point
         out[nm] = {"status": cpd.STATUS[r["status"]], "iterations": r["iterations"], "seconds": r["wall_s"],
-                   "it_per_s": r["iterations"] / r["wall_s"], "corner_iterations": rc["iterations"],
+                   "it_per_s": r["iterations"] / r["wall_s"], "corner_status": cpd.STATUS[rc["status"]],
+                   "corner_iterations": rc["iterations"],
                    "corner_seconds": rc["wall_s"]}
         S.close()
         P.close()

@@ -203,6 +203,43 @@ int cpd_solver_counters(const cpd_solver *s, int64_t out[4]);
 /* Algorithmic bytes one launch of kernel `name` moves (DESIGN.md byte model). */
 int cpd_kernel_bytes(const cpd_solver *s, const char *name, double *bytes);
 
+/* ------------------------------------------------------------------ multi-GPU
+ * One process per GPU.  The LP is split into
+ * contiguous blocks balanced by nonzeros (+1 per row for the vector work):
+ *   partition 0 = row-block (BJ north_star): rank p keeps rows R_p of A; y, b, Ax
+ *     are sharded with them; A^T y is partial on every rank and is reduce-scattered
+ *     into equal slices of length L = ceil(n / world) of the n-side, where the
+ *     primal step runs; x+ is all-gathered for the local A x+.
+ *   partition 1 = col-block: rank p keeps columns C_p; x, c, bounds are sharded;
+ *     A x+ is partial, reduce-scattered into slices of the m-side where the dual
+ *     step runs; y+ is all-gathered for the local A^T y.
+ *   partition -1 = col-block if n >= m else row-block ("shard the long vector").
+ * Every scalar the device decisions use is allreduced first, so all ranks take
+ * the same decisions.  All calls on a distributed problem or its solvers are
+ * COLLECTIVE: every rank makes them in the same order.  cpd_get_iterate /
+ * cpd_set_iterate / cpd_problem_score / cpd_compute_stats take and return GLOBAL
+ * vectors; cpd_problem_info reports global m, n and LOCAL nnz. */
+
+/* Host-only (no device needed): bounds[world + 1] of the contiguous blocks of
+ * columns (partition 1) or rows (partition 0) this library assigns to each rank,
+ * from the GLOBAL CSR(A^T).  CPD_E_ARG if world > min(m, n). */
+int cpd_partition(int32_t m, int32_t n, const int32_t *AT_rowptr, const int32_t *AT_col, int32_t world,
+                  int32_t partition, int64_t *bounds);
+/* 128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it). */
+int cpd_nccl_get_unique_id(char id[128]);
+/* Create this rank's block of the GLOBAL LP (CSR(A^T) + b, c, lb, ub, all in host
+ * memory, borrowed for the call) on `device`, and the NCCL communicator of
+ * `world` ranks from `id`.  Validation as cpd_problem_create, on the block. */
+int cpd_problem_create_dist(int32_t rank, int32_t world, const char id[128], int32_t partition,
+                            int32_t m, int32_t n, int64_t nnz,
+                            const int32_t *AT_rowptr, const int32_t *AT_col, const double *AT_val,
+                            const double *b, const double *c, const double *lb, const double *ub,
+                            int32_t device, cpd_problem **out);
+/* info = {world, rank, partition (-1 single GPU), L, owned m-side length, owned
+ * n-side length, global index of the first owned m-side / n-side element, local
+ * rows of A, local rows of A^T}. */
+int cpd_problem_dist_info(const cpd_problem *p, int64_t info[10]);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

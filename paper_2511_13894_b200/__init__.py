@@ -31,6 +31,7 @@ DECLARED_SYMBOLS = [
     "cpd_solve", "cpd_corner_push", "cpd_step", "cpd_get_iterate", "cpd_set_iterate", "cpd_get_stats",
     "cpd_get_trajectory", "cpd_power_sigma", "cpd_problem_score", "cpd_compute_stats",
     "cpd_get_kernel_times", "cpd_kernel_bytes", "cpd_solver_counters",
+    "cpd_partition", "cpd_nccl_get_unique_id", "cpd_problem_create_dist", "cpd_problem_dist_info",
 ]
 
 
@@ -110,6 +111,11 @@ def lib():
             "cpd_get_kernel_times": (C.c_int, [P, P, P, P, I32, C.POINTER(I32), I32]),
             "cpd_kernel_bytes": (C.c_int, [P, C.c_char_p, C.POINTER(D)]),
             "cpd_solver_counters": (C.c_int, [P, P]),
+            "cpd_partition": (C.c_int, [I32, I32, P, P, I32, I32, P]),
+            "cpd_nccl_get_unique_id": (C.c_int, [C.c_char_p]),
+            "cpd_problem_create_dist": (C.c_int, [I32, I32, C.c_char_p, I32, I32, I32, I64, P, P, P, P, P, P,
+                                                  P, I32, C.POINTER(P)]),
+            "cpd_problem_dist_info": (C.c_int, [P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -155,6 +161,23 @@ def cpd_corner_params_default(**kw) -> CornerParams:
     for k, v in kw.items():
         setattr(p, k, v)
     return p
+
+
+def partition(m, n, ATp, ATj, world, partition):
+    """cpd_partition: block bounds [world + 1] (host only, no device needed)."""
+    ATp = np.ascontiguousarray(ATp, np.int32)
+    ATj = np.ascontiguousarray(ATj, np.int32)
+    out = np.zeros(world + 1, np.int64)
+    _check(lib().cpd_partition(int(m), int(n), ATp.ctypes.data, ATj.ctypes.data, int(world), int(partition),
+                               out.ctypes.data))
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    """cpd_nccl_get_unique_id: 128 bytes, to be broadcast to every rank by the caller."""
+    buf = C.create_string_buffer(128)
+    _check(lib().cpd_nccl_get_unique_id(buf))
+    return buf.raw
 
 
 class Problem:
@@ -206,6 +229,31 @@ class Problem:
             A = tuple(conv(a) for a in A) if A else None
             vecs = {k: conv(v) for k, v in vecs.items()}
         return cls(lp.m, lp.n, A=A, AT=AT, device=device, **vecs)
+
+    @classmethod
+    def create_dist(cls, lp, rank, world, uid: bytes, partition=-1, device=0):
+        """cpd_problem_create_dist: this rank's block of the GLOBAL LP (host arrays)."""
+        self = cls.__new__(cls)
+        self.m, self.n = int(lp.m), int(lp.n)
+        arrs = [np.ascontiguousarray(lp.ATp, np.int32), np.ascontiguousarray(lp.ATj, np.int32),
+                np.ascontiguousarray(lp.ATx, np.float64)]
+        vecs = [np.ascontiguousarray(v, np.float64) if v is not None else None for v in (lp.b, lp.c, lp.lb, lp.ub)]
+        ptrs = [a.ctypes.data for a in arrs] + [v.ctypes.data if v is not None else None for v in vecs]
+        h = C.c_void_p()
+        idb = C.create_string_buffer(bytes(uid), 128)
+        _check(lib().cpd_problem_create_dist(int(rank), int(world), idb, int(partition), self.m, self.n,
+                                             int(lp.ATp[-1]), *ptrs, int(device), C.byref(h)))
+        self.h = h
+        self.nnz = int(lp.ATp[-1])
+        self.mem = HOST
+        return self
+
+    def dist_info(self):
+        out = (C.c_int64 * 10)()
+        _check(lib().cpd_problem_dist_info(self.h, out))
+        keys = ("world", "rank", "partition", "L", "own_m", "own_n", "gofs_m", "gofs_n", "local_rows_A",
+                "local_rows_AT")
+        return dict(zip(keys, list(out)))
 
     def info(self):
         out = (C.c_int64 * 8)()

@@ -9,7 +9,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libcpd.so")
+# CPD_LIB: load/build another library file (tuning experiments only; default in-tree libcpd.so)
+LIB = os.environ.get("CPD_LIB", os.path.join(PKG, "libcpd.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -48,11 +49,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc, nlib = _nccl_dirs()
     extra_inc = ["-I" + os.path.join(ROOT, "include")] + (["-I" + inc] if inc else [])
     defs = ["-DCPD_HAVE_NCCL=1"] if inc else []
-    build_dir = os.path.join(PKG, "build")
+    build_dir = os.path.join(PKG, "build" + os.environ.get("CPD_BUILD_TAG", ""))
     os.makedirs(build_dir, exist_ok=True)
     for src in sources():
         obj = os.path.join(build_dir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *extra_inc, *defs, "-c", src, "-o", obj]
+        extra = os.environ.get("CPD_NVCC_DEFS", "").split()
+        cmd = [NVCC, *ARCH, *FLAGS, *extra_inc, *defs, *extra, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode:
             sys.stderr.write(r.stdout + r.stderr)

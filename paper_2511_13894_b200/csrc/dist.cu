@@ -1,0 +1,267 @@
+// dist.cu — multi-GPU plumbing: partition of the LP
+// over ranks, extraction of this rank's block, the NCCL communicator and the
+// collectives the passes use.  One process per GPU; the 128-byte NCCL id is
+// broadcast by the caller (torch.distributed), so the library needs no launcher.
+//
+// Scheme ("shard the long vector, exchange the short one"):
+//   partition 0 = row-block (north_star): rank p keeps rows R_p of A (nnz-balanced),
+//       y/b/Ax sharded with them; A^T y is partial on every rank -> reduce-scatter
+//       into equal slices of the n-side, primal step on the slice, all-gather x+.
+//   partition 1 = col-block: rank p keeps columns C_p (nnz-balanced), x/c/bounds
+//       sharded with them; A x+ is partial -> reduce-scatter into equal slices of
+//       the m-side, dual step on the slice, all-gather y+.
+// Scalars (norms, dots, counts) are allreduced before every device decision.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+#ifdef CPD_HAVE_NCCL
+#include <nccl.h>
+#endif
+
+cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const int32_t* Ap,
+                                     const int32_t* Aj, const double* Ax, const int32_t* ATp,
+                                     const int32_t* ATj, const double* ATx, const double* b,
+                                     const double* c, const double* lb, const double* ub,
+                                     int32_t mem, int32_t device);
+
+namespace cpd {
+
+#ifdef CPD_HAVE_NCCL
+#define CPD_NCCL(call)                                                                        \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess) throw ::cpd::Error(CPD_E_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+static ncclComm_t comm_of(const cpd_problem* P) { return (ncclComm_t)P->comm; }
+#endif
+
+void dist_destroy(cpd_problem* P)
+{
+#ifdef CPD_HAVE_NCCL
+    if (P->comm) ncclCommDestroy((ncclComm_t)P->comm);
+#endif
+    P->comm = nullptr;
+}
+
+void Ctx::allreduce_sum(double* buf, int64_t count)
+{
+    if (P->split < 0) return;
+#ifdef CPD_HAVE_NCCL
+    CPD_NCCL(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, comm_of(P), st));
+#else
+    throw Error(CPD_E_NCCL, "built without NCCL");
+#endif
+}
+
+void Ctx::allreduce_max_host(double* v)
+{
+    if (P->split < 0) return;
+#ifdef CPD_HAVE_NCCL
+    DBuf<double> d(1);
+    CPD_CUDA(cudaMemcpyAsync(d.p, v, sizeof(double), cudaMemcpyHostToDevice, st));
+    CPD_NCCL(ncclAllReduce(d.p, d.p, 1, ncclDouble, ncclMax, comm_of(P), st));
+    CPD_CUDA(cudaMemcpyAsync(v, d.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CPD_CUDA(cudaStreamSynchronize(st));
+#endif
+}
+
+void Ctx::reduce_scatter(const double* send, double* rv, int64_t count)
+{
+#ifdef CPD_HAVE_NCCL
+    CPD_NCCL(ncclReduceScatter(send, rv, (size_t)count, ncclDouble, ncclSum, comm_of(P), st));
+#else
+    throw Error(CPD_E_NCCL, "built without NCCL");
+#endif
+}
+
+void Ctx::all_gather_inplace(double* buf, int64_t count)
+{
+#ifdef CPD_HAVE_NCCL
+    CPD_NCCL(ncclAllGather(buf + (int64_t)P->rank * count, buf, (size_t)count, ncclDouble, comm_of(P), st));
+#else
+    throw Error(CPD_E_NCCL, "built without NCCL");
+#endif
+}
+
+void Ctx::all_gather(const double* send, double* rv, int64_t count)
+{
+#ifdef CPD_HAVE_NCCL
+    CPD_NCCL(ncclAllGather(send, rv, (size_t)count, ncclDouble, comm_of(P), st));
+#else
+    throw Error(CPD_E_NCCL, "built without NCCL");
+#endif
+}
+
+// Contiguous blocks of rows with weights w_r = len_r + 1 (nonzeros plus the
+// row's vector work), balanced: bounds[q] = first row whose prefix weight reaches
+// q W / world; every block non-empty.
+static std::vector<int64_t> balanced_blocks(const std::vector<int64_t>& len, int world)
+{
+    const int64_t R = (int64_t)len.size();
+    std::vector<int64_t> pre(R + 1, 0);
+    for (int64_t r = 0; r < R; ++r) pre[r + 1] = pre[r] + len[r] + 1;
+    const double W = (double)pre[R];
+    std::vector<int64_t> bnd(world + 1, 0);
+    bnd[world] = R;
+    for (int q = 1; q < world; ++q) {
+        const double target = W * q / world;
+        int64_t r = std::lower_bound(pre.begin(), pre.end(), (int64_t)std::ceil(target)) - pre.begin();
+        r = std::max<int64_t>(r, bnd[q - 1] + 1);
+        r = std::min<int64_t>(r, R - (world - q));
+        bnd[q] = r;
+    }
+    return bnd;
+}
+
+}  // namespace cpd
+
+using namespace cpd;
+
+static thread_local std::string g_derr;
+
+extern "C" {
+
+/* see include/cpd.h */
+int cpd_partition(int32_t m, int32_t n, const int32_t* AT_rowptr, const int32_t* AT_col, int32_t world,
+                  int32_t partition, int64_t* bounds)
+{
+    try {
+        if (!AT_rowptr || !bounds || world < 1 || m < 1 || n < 1 || (partition != 0 && partition != 1))
+            return CPD_E_ARG;
+        if (world > std::min(m, n)) return CPD_E_ARG;
+        std::vector<int64_t> len;
+        if (partition == 1) {   // column blocks: column j = row j of A^T
+            len.resize(n);
+            for (int32_t j = 0; j < n; ++j) len[j] = (int64_t)AT_rowptr[j + 1] - AT_rowptr[j];
+        } else {                // row blocks: row counts of A
+            if (!AT_col && AT_rowptr[n] > 0) return CPD_E_ARG;
+            len.assign(m, 0);
+            const int64_t nnz = AT_rowptr[n];
+            for (int64_t q = 0; q < nnz; ++q) {
+                const int32_t i = AT_col[q];
+                if (i < 0 || i >= m) return CPD_E_CSR;
+                len[i] += 1;
+            }
+        }
+        const std::vector<int64_t> b = balanced_blocks(len, world);
+        std::copy(b.begin(), b.end(), bounds);
+    } catch (...) {
+        return CPD_E_ARG;
+    }
+    return CPD_OK;
+}
+
+int cpd_nccl_get_unique_id(char id[128])
+{
+#ifdef CPD_HAVE_NCCL
+    if (!id) return CPD_E_ARG;
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) return CPD_E_NCCL;
+    static_assert(sizeof(u) == 128, "NCCL unique id is 128 bytes");
+    std::memcpy(id, &u, 128);
+    return CPD_OK;
+#else
+    (void)id;
+    return CPD_E_NCCL;
+#endif
+}
+
+}  // extern "C"
+
+// Called from the ABI layer in solver.cu (error text via its cpd_last_error).
+cpd_problem* cpd_problem_create_dist_impl(int32_t rank, int32_t world, const char id[128], int32_t partition,
+                                          int32_t m, int32_t n, int64_t nnz, const int32_t* ATp,
+                                          const int32_t* ATj, const double* ATx, const double* b,
+                                          const double* c, const double* lb, const double* ub, int32_t device)
+{
+    if (world < 1 || rank < 0 || rank >= world) throw Error(CPD_E_ARG, "need 0 <= rank < world");
+    if (m < 1 || n < 1 || nnz < 0 || nnz >= (1LL << 31)) throw Error(CPD_E_DIM, "need m >= 1, n >= 1, 0 <= nnz < 2^31");
+    if (world > std::min(m, n)) throw Error(CPD_E_DIM, "world size exceeds min(m, n)");
+    if (!ATp || (nnz > 0 && (!ATj || !ATx)) || !b || !c || !id) throw Error(CPD_E_ARG, "NULL argument");
+    if ((int64_t)ATp[n] != nnz || ATp[0] != 0) throw Error(CPD_E_CSR, "AT_rowptr does not span [0, nnz]");
+    if (partition < 0) partition = (n >= m) ? 1 : 0;   // shard the long side
+    if (partition > 1) throw Error(CPD_E_ARG, "partition must be -1, 0 (row-block) or 1 (col-block)");
+    std::vector<int64_t> bnd(world + 1);
+    int rc = cpd_partition(m, n, ATp, ATj, world, partition, bnd.data());
+    if (rc != CPD_OK) throw Error(rc, "partition failed (bad CSR(A^T))");
+    const int split = partition == 0 ? 1 : 0;
+    const int64_t rows_split = split == 1 ? n : m;
+    const int64_t L = (rows_split + world - 1) / world;
+    const int64_t b0 = bnd[rank], b1 = bnd[rank + 1];
+
+    cpd_problem* P = nullptr;
+    if (partition == 1) {
+        // columns [b0, b1): rows b0..b1 of CSR(A^T), global row indices of A
+        std::vector<int32_t> p((size_t)(b1 - b0) + 1);
+        for (int64_t j = b0; j <= b1; ++j) p[j - b0] = ATp[j] - ATp[b0];
+        const int64_t nz = p.back();
+        P = cpd_problem_create_impl(m, (int32_t)(b1 - b0), nz, nullptr, nullptr, nullptr, p.data(),
+                                    nz ? ATj + ATp[b0] : nullptr, nz ? ATx + ATp[b0] : nullptr, b, c + b0,
+                                    lb ? lb + b0 : nullptr, ub ? ub + b0 : nullptr, CPD_HOST, device);
+    } else {
+        // rows [b0, b1) of A: keep those entries of every column, local row index
+        std::vector<int32_t> p((size_t)n + 1, 0), j;
+        std::vector<double> x;
+        for (int32_t col = 0; col < n; ++col) {
+            for (int64_t q = ATp[col]; q < ATp[col + 1]; ++q) {
+                const int32_t i = ATj[q];
+                if (i >= b0 && i < b1) {
+                    j.push_back((int32_t)(i - b0));
+                    x.push_back(ATx[q]);
+                }
+            }
+            p[col + 1] = (int32_t)j.size();
+        }
+        const int64_t nz = (int64_t)j.size();
+        P = cpd_problem_create_impl((int32_t)(b1 - b0), n, nz, nullptr, nullptr, nullptr, p.data(),
+                                    nz ? j.data() : nullptr, nz ? x.data() : nullptr, b + b0, c, lb, ub, CPD_HOST,
+                                    device);
+    }
+    try {
+        P->world = world;
+        P->rank = rank;
+        P->split = split;
+        P->m_glob = m;
+        P->n_glob = n;
+        P->L = L;
+        const int local = 1 - split;   // the side with nnz-balanced blocks
+        for (int s = 0; s < 2; ++s) {
+            P->rank_gofs[s].assign(world, 0);
+            P->rank_len[s].assign(world, 0);
+            for (int q = 0; q < world; ++q) {
+                if (s == split) {
+                    const int64_t o = std::min<int64_t>((int64_t)q * L, rows_split);
+                    P->rank_gofs[s][q] = o;
+                    P->rank_len[s][q] = std::min<int64_t>(L, rows_split - o);
+                } else {
+                    P->rank_gofs[s][q] = bnd[q];
+                    P->rank_len[s][q] = bnd[q + 1] - bnd[q];
+                }
+            }
+            P->own_len[s] = (int32_t)P->rank_len[s][rank];
+            P->gofs[s] = P->rank_gofs[s][rank];
+            P->poff[s] = (s == split) ? P->gofs[s] : 0;   // the local problem holds all rows of the split side
+        }
+        (void)local;
+#ifdef CPD_HAVE_NCCL
+        ncclUniqueId u;
+        std::memcpy(&u, id, 128);
+        ncclComm_t comm;
+        CPD_CUDA(cudaSetDevice(device));
+        CPD_NCCL(ncclCommInitRank(&comm, world, u, rank));
+        P->comm = comm;
+#else
+        throw Error(CPD_E_NCCL, "built without NCCL");
+#endif
+    } catch (...) {
+        delete P;
+        throw;
+    }
+    return P;
+}
+
+cpd_problem::~cpd_problem() { cpd::dist_destroy(this); }

@@ -92,11 +92,35 @@ struct cpd_problem {
     bool uniform_bounds = false;
     double l0 = 0.0, u0 = 0.0;
     int num_sms = 148;
+    // ---- distribution.  Side 0 = m-side (rows of A: y, b, Ax),
+    // side 1 = n-side (rows of A^T: x, c, bounds).  The local matrices are this
+    // rank's block: row-block (split = 1) keeps rows R_p of A, so A has m_p rows and
+    // A^T all n rows; col-block (split = 0) keeps columns C_p, so A^T has n_p rows
+    // and A all m rows.  The side whose local rows are ALL rows is the split side:
+    // its products are partial, reduce-scattered into equal slices of length L, and
+    // its state vectors hold only the owned slice.  world == 1: split = -1.
+    int world = 1, rank = 0, split = -1;
+    int32_t m_glob = 0, n_glob = 0;
+    int32_t own_len[2] = {0, 0};     // owned length of each side's state vectors
+    int64_t poff[2] = {0, 0};        // offset of the owned part in this problem's b / c, lb, ub
+    int64_t gofs[2] = {0, 0};        // global index of owned element 0
+    int64_t L = 0;                   // slice length of the split side
+    std::vector<int64_t> rank_gofs[2], rank_len[2];   // every rank's owned part (global)
+    void* comm = nullptr;            // ncclComm_t (split >= 0)
     cpd::Bounds bounds() const
     {
         if (uniform_bounds) return cpd::Bounds{nullptr, nullptr, l0, u0};
         return cpd::Bounds{lb.p, ub.p, 0.0, 0.0};
     }
+    // bounds of the owned n-side part
+    cpd::Bounds bounds_own() const
+    {
+        if (uniform_bounds) return cpd::Bounds{nullptr, nullptr, l0, u0};
+        return cpd::Bounds{lb.p + poff[1], ub.p + poff[1], 0.0, 0.0};
+    }
+    const double* b_own() const { return b.p + poff[0]; }
+    const double* c_own() const { return c.p + poff[1]; }
+    ~cpd_problem();
 };
 
 namespace cpd {
@@ -114,6 +138,8 @@ struct Ctx {
     DBuf<double> bpart;
     DBuf<unsigned> ctr;
     DBuf<double> lpartA, lpartAT;     // long-row piece partials of each layout
+    DBuf<double> red;                 // this rank's totals of the last reduction (distributed)
+    DBuf<double> part, recv;          // reduce-scatter send [world][2][L] / receive [2][L] buffers
     int grid_elem = 0;
     int64_t launches = 0;            // kernels of this library launched on `st` (graph nodes included)
     explicit Ctx(const cpd_problem* p);
@@ -127,6 +153,12 @@ struct Ctx {
     void sync();
     template <class F>
     int grid_for(F kernel);
+    // collectives on the problem's communicator, on `st` (no-ops when split < 0)
+    void allreduce_sum(double* buf, int64_t count);
+    void allreduce_max_host(double* v);                // host scalar, synchronous
+    void reduce_scatter(const double* send, double* recv, int64_t count);
+    void all_gather_inplace(double* buf, int64_t count);   // buf[world * count], own chunk at rank * count
+    void all_gather(const double* send, double* recv, int64_t count);
 };
 
 // Launch helpers (templates instantiated in solver.cu).
@@ -140,8 +172,11 @@ struct AuxScope {
 
 template <int NV, class Epi>
 void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel v1, const Epi& epi,
-                 Gate g);
+                 Gate g, double* red = nullptr);
 template <class Op>
-void launch_elem(Ctx& cx, int64_t N, const Op& op, Gate g);
+void launch_elem(Ctx& cx, int64_t N, const Op& op, Gate g, double* red = nullptr);
+
+// distributed problem plumbing (dist.cu)
+void dist_destroy(cpd_problem* P);
 
 }  // namespace cpd

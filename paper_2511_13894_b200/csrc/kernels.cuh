@@ -218,7 +218,7 @@ __device__ __forceinline__ void block_sum(double (&v)[NS], double (*sw)[NS])
 // (the rows kernel of a plan with long rows), or 0.
 template <int NS, int NT = TPB, class Fin>
 __device__ __forceinline__ void grid_finalize(double (&acc)[NS], double* bpart, unsigned* ctr, int prev,
-                                              Fin fin)
+                                              double* red, Fin fin)
 {
     __shared__ double sw[NT / 32][NS];
     __shared__ int s_last;
@@ -242,7 +242,12 @@ __device__ __forceinline__ void grid_finalize(double (&acc)[NS], double* bpart, 
         for (int s = 0; s < NS; ++s) tot[s] += __ldcg(&bpart[(size_t)b * NS + s]);
     block_sum<NS, NT>(tot, sw);
     if (threadIdx.x == 0) {
-        fin(tot);
+        if (red) {   // distributed: this rank's totals; summed over ranks, then k_fin
+#pragma unroll
+            for (int s = 0; s < NS; ++s) red[s] = tot[s];
+        } else {
+            fin(tot);
+        }
         *ctr = 0u;
         __threadfence();
     }
@@ -327,7 +332,10 @@ constexpr int TPB_SP = (NCW + 1) * 32;    // + one TMA producer warp
 constexpr int NGRP = 2;                   // long-row pieces rotate over NGRP groups of consumer warps
 constexpr int GW = NCW / NGRP;            // warps per group
 constexpr int WCHUNK = CAP / GW;          // nonzeros per warp share of a long-row piece (8 per lane)
-constexpr size_t SMEM_BUDGET = 220 * 1024;
+#ifndef CPD_SMEM_KB
+#define CPD_SMEM_KB 220
+#endif
+constexpr size_t SMEM_BUDGET = CPD_SMEM_KB * 1024;   // shared memory of the stage ring (rest is L1)
 
 template <int NV, int NVEC>
 struct StageSet {
@@ -584,7 +592,7 @@ __device__ __forceinline__ bool consume_entry(SpmvSmem<NV, Epi::NVEC>& S, int s,
 template <int NV, class Epi>
 __global__ void __launch_bounds__(TPB_SP, 1)
 k_spmv(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* bpart,
-       unsigned* ctr)
+       unsigned* ctr, double* red)
 {
     constexpr int NS = Epi::NS;
     constexpr int NVEC = Epi::NVEC;
@@ -651,7 +659,7 @@ k_spmv(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
         }
     }
     if (P.nlong == 0)
-        grid_finalize<NS, TPB_SP>(acc, bpart, ctr, 0, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+        grid_finalize<NS, TPB_SP>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
     else
         block_partial<NS, TPB_SP>(acc, bpart);
 }
@@ -662,7 +670,7 @@ k_spmv(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
 // (first `prev` slots) and finalizes.
 template <int NV, class Epi>
 __global__ void __launch_bounds__(TPB)
-k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, int prev)
+k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, int prev, double* red)
 {
     constexpr int NS = Epi::NS;
     constexpr int NVEC = Epi::NVEC;
@@ -693,13 +701,13 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
             e.row(r, sm, vin, r, acc);
         }
     }
-    grid_finalize<NS>(acc, bpart, ctr, prev, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+    grid_finalize<NS>(acc, bpart, ctr, prev, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
 }
 
 // Elementwise pass over [0, N) with reductions and a device-side finalize.
 template <class Op>
 __global__ void __launch_bounds__(TPB)
-k_elem(int64_t N, Op op, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr)
+k_elem(int64_t N, Op op, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, double* red)
 {
     constexpr int NS = Op::NS;
     __shared__ int s_go;
@@ -716,7 +724,83 @@ k_elem(int64_t N, Op op, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr)
     for (int s = 0; s < NS; ++s) acc[s] = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < N; i += (int64_t)gridDim.x * TPB)
         o.elem(i, acc);
-    grid_finalize<NS>(acc, bpart, ctr, 0, [o, ctl](double* tot) { o.finalize(tot, ctl); });
+    grid_finalize<NS>(acc, bpart, ctr, 0, red, [o, ctl](double* tot) { o.finalize(tot, ctl); });
+}
+
+// ------------------------------------------------------------ distributed helpers
+// Owned-slice epilogue of a split product: the row sums of rows [0, N) of this
+// rank's slice arrive reduce-scattered in recv[v * L + i] (v < NV); each is handed
+// to the same fused epilogue the single-GPU kernel applies.
+template <int NV, class Epi>
+__global__ void __launch_bounds__(TPB)
+k_slice(int64_t N, int64_t L, const double* __restrict__ recv, Epi epi, Gate gate, Ctl* ctl, double* bpart,
+        unsigned* ctr, double* red)
+{
+    constexpr int NS = Epi::NS;
+    constexpr int NVEC = Epi::NVEC;
+    __shared__ int s_go;
+    if (threadIdx.x == 0) s_go = gate_open(gate, ctl);
+    __syncthreads();
+    if (!s_go) return;
+    Epi e = epi;
+    e.load(ctl);
+    const double* vin[NVEC > 0 ? NVEC : 1];
+#pragma unroll
+    for (int v = 0; v < NVEC; ++v) vin[v] = e.vec(v);
+    double acc[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < N; i += (int64_t)gridDim.x * TPB) {
+        double sm[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sm[v] = recv[v * L + i];
+        e.row((int)i, sm, vin, (int)i, acc);
+    }
+    grid_finalize<NS>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+}
+
+// Device finalize of an epilogue on totals summed over ranks (red, after the
+// scalar allreduce); same gate as the kernel whose totals these are.
+template <class Epi>
+__global__ void k_fin(Epi epi, Gate gate, Ctl* ctl, const double* red)
+{
+    if (!gate_open(gate, ctl)) return;
+    double tot[Epi::NS];
+#pragma unroll
+    for (int s = 0; s < Epi::NS; ++s) tot[s] = red[s];
+    epi.finalize(tot, ctl);
+}
+
+// Split product: row r's NV sums go to the reduce-scatter send buffer, laid out
+// [owner q = r / L][v][r - q L] so that rank q receives [v][L].
+template <int NV_>
+struct EpiStore {
+    static constexpr int NS = 1;
+    static constexpr int NVEC = 0;
+    double* part;
+    int64_t L;
+    __device__ void load(const Ctl*) {}
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
+    __device__ __forceinline__ void row(int r, const double* s, const double* const*, int, double*) const
+    {
+        const int64_t q = r / L;
+        double* d = part + q * NV_ * L + (r - q * L);
+#pragma unroll
+        for (int v = 0; v < NV_; ++v) d[v * L] = s[v];
+    }
+    __device__ void finalize(const double*, Ctl*) const {}
+};
+
+// Replica refresh: dst[i] = src(k)[i] for i < N (the owned slice, copied into its
+// place in the all-gather buffer).
+static __global__ void __launch_bounds__(TPB) k_copy_sel(int64_t N, double* dst, VecSel src, Gate gate, Ctl* ctl)
+{
+    __shared__ int s_go;
+    if (threadIdx.x == 0) s_go = gate_open(gate, ctl);
+    __syncthreads();
+    if (!s_go) return;
+    const double* s = src.get(ctl);
+    for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < N; i += (int64_t)gridDim.x * TPB) dst[i] = s[i];
 }
 
 // ------------------------------------------------------------ epilogues
@@ -1114,10 +1198,11 @@ struct OpPowInit {
     double* v;
     uint64_t seed;
     int32_t n;
+    int64_t jbase = 0;   // global index of local column 0 (distributed problems)
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ void elem(int64_t j, double* acc) const
     {
-        const double x = u01(seed, j) - 0.5;
+        const double x = u01(seed, jbase + j) - 0.5;
         v[j] = x;
         acc[0] += x * x;
     }
@@ -1168,6 +1253,7 @@ struct EpiCorner {
     const double* obj;   // caller objective (device copy) or null
     double eps_abs, obj_scale;
     uint64_t seed;
+    int64_t jbase = 0;   // global index of local column 0 (distributed problems)
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ void row(int j, const double* s, const double* const*, int, double* acc) const
     {
@@ -1176,7 +1262,7 @@ struct EpiCorner {
         const double xj = x[j];
         if (zj < -eps_abs) { lhat[j] = xj; acc[0] += 1.0; } else lhat[j] = bd.lo(j);
         if (zj > eps_abs) { uhat[j] = xj; acc[1] += 1.0; } else uhat[j] = bd.hi(j);
-        chat[j] = obj ? obj[j] : obj_scale * u01(seed, j);
+        chat[j] = obj ? obj[j] : obj_scale * u01(seed, jbase + j);
     }
     __device__ void finalize(const double* tot, Ctl* ctl) const
     {

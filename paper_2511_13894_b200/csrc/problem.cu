@@ -349,6 +349,15 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         P->m = m;
         P->n = n;
         P->nnz = nnz;
+        // single-GPU layout (cpd_problem_create_dist overrides these)
+        P->m_glob = m;
+        P->n_glob = n;
+        P->own_len[0] = m;
+        P->own_len[1] = n;
+        P->rank_gofs[0] = {0};
+        P->rank_gofs[1] = {0};
+        P->rank_len[0] = {m};
+        P->rank_len[1] = {n};
         CPD_CUDA(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, device));
         const int sms = P->num_sms;
         DBuf<unsigned long long> err(NERR);

@@ -1,4 +1,4 @@
-// solver.cu — the R-PDHG run state machine,
+// solver.cu — the R-PDHG run state machine (DESIGN.md §6 "Schedule"),
 // Algorithm 1 orchestration, statistics, stand-alone entry points and
 // the extern "C" ABI of include/cpd.h.
 //
@@ -8,6 +8,13 @@
 // launched as ONE CUDA graph; every node reads the device control block and
 // either does its work or returns at once (gates), so the same graph serves every
 // batch and the host synchronises once per K iterations.
+//
+// Distributed problems: every pass goes through pass<NV>(side, ...):
+// the side whose rows are split runs the SpMV into a partial buffer, reduce-
+// scatters it and applies the same fused epilogue to the owned slice; scalar
+// totals are allreduced and the device decision (k_fin) runs on the sums, so all
+// ranks take identical decisions.  With one GPU (split < 0) pass<> is exactly
+// the single fused kernel with its last-CTA finalize.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -42,6 +49,14 @@ Ctx::Ctx(const cpd_problem* p) : P(p)
     const Plan& pt = p->AT.plan;
     lpartA.alloc((size_t)std::max<int64_t>(1, pa.long_pieces) * GW * 2);
     lpartAT.alloc((size_t)std::max<int64_t>(1, pt.long_pieces) * GW * 2);
+    red.alloc(NSMAX);
+    CPD_CUDA(cudaMemset(red.p, 0, sizeof(double) * NSMAX));
+    if (p->split >= 0) {
+        part.alloc((size_t)p->world * 2 * p->L);
+        recv.alloc((size_t)2 * p->L);
+        CPD_CUDA(cudaMemset(part.p, 0, sizeof(double) * p->world * 2 * p->L));
+        CPD_CUDA(cudaMemset(recv.p, 0, sizeof(double) * 2 * p->L));
+    }
     grid_elem = p->num_sms * 4;
 }
 
@@ -100,7 +115,7 @@ static std::mutex g_grid_mu;
 
 template <int NV, class Epi>
 void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel v1, const Epi& epi,
-                 Gate g)
+                 Gate g, double* red)
 {
     constexpr size_t SMEM = sizeof(SpmvSmem<NV, Epi::NVEC>);
     static int grid = 0, sms = 0;
@@ -117,49 +132,146 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         }
     }
     const int gr = std::max(1, std::min(grid, dp.nent));
-    k_spmv<NV, Epi><<<gr, TPB_SP, SMEM, cx.st>>>(M.dev(), dp, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p);
+    k_spmv<NV, Epi><<<gr, TPB_SP, SMEM, cx.st>>>(M.dev(), dp, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p,
+                                                 red);
     CPD_CUDA(cudaGetLastError());
     ++cx.launches;
     if (dp.nlong > 0) {
         const int gf = std::max(1, std::min(cx.P->num_sms * 8, dp.nlong));
         Gate g2 = g;
         g2.active = nullptr;
-        k_finish<NV, Epi><<<gf, TPB, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, gr);
+        k_finish<NV, Epi><<<gf, TPB, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, gr, red);
         CPD_CUDA(cudaGetLastError());
         ++cx.launches;
     }
 }
 
 template <class Op>
-void launch_elem(Ctx& cx, int64_t N, const Op& op, Gate g)
+void launch_elem(Ctx& cx, int64_t N, const Op& op, Gate g, double* red)
 {
     const int64_t need = (N + TPB - 1) / TPB;
     const int gr = (int)std::max<int64_t>(1, std::min<int64_t>(need, cx.grid_elem));
-    k_elem<Op><<<gr, TPB, 0, cx.st>>>(N, op, g, cx.ctl, cx.bpart.p, cx.ctr.p);
+    k_elem<Op><<<gr, TPB, 0, cx.st>>>(N, op, g, cx.ctl, cx.bpart.p, cx.ctr.p, red);
     CPD_CUDA(cudaGetLastError());
     ++cx.launches;
+}
+
+template <class Epi>
+static void launch_fin(Ctx& cx, const Epi& e, Gate g)
+{
+    g.active = nullptr;
+    k_fin<Epi><<<1, 1, 0, cx.st>>>(e, g, cx.ctl, cx.red.p);
+    CPD_CUDA(cudaGetLastError());
+    ++cx.launches;
+}
+
+// One epilogue pass over side `side` (0: rows of A, m-side; 1: rows of A^T, n-side).
+template <int NV, class Epi>
+static void pass(Ctx& cx, int side, VecSel v0, VecSel v1, const Epi& epi, Gate g)
+{
+    const cpd_problem* P = cx.P;
+    const Matrix& M = side ? P->AT : P->A;
+    const DevPlan dp = side ? cx.planAT() : cx.planA();
+    if (P->split < 0) {
+        launch_spmv<NV>(cx, M, dp, v0, v1, epi, g, nullptr);
+        return;
+    }
+    if (P->split == side) {
+        EpiStore<NV> es{cx.part.p, P->L};
+        launch_spmv<NV>(cx, M, dp, v0, v1, es, g, nullptr);
+        cx.reduce_scatter(cx.part.p, cx.recv.p, (int64_t)NV * P->L);
+        const int64_t N = P->own_len[side];
+        const int gr = (int)std::max<int64_t>(1, std::min<int64_t>((N + TPB - 1) / TPB, cx.grid_elem));
+        Gate g2 = g;
+        g2.active = nullptr;
+        k_slice<NV, Epi><<<gr, TPB, 0, cx.st>>>(N, P->L, cx.recv.p, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p,
+                                                cx.red.p);
+        CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
+    } else {
+        launch_spmv<NV>(cx, M, dp, v0, v1, epi, g, cx.red.p);
+    }
+    cx.allreduce_sum(cx.red.p, Epi::NS);
+    launch_fin(cx, epi, g);
+}
+
+// Elementwise pass over the owned parts; `reduce` = the op's totals matter.
+template <class Op>
+static void elem(Ctx& cx, int64_t N, const Op& op, Gate g, bool reduce)
+{
+    const cpd_problem* P = cx.P;
+    if (P->split < 0) {
+        launch_elem(cx, N, op, g, nullptr);
+        return;
+    }
+    launch_elem(cx, N, op, g, cx.red.p);
+    if (reduce) {
+        cx.allreduce_sum(cx.red.p, Op::NS);
+        launch_fin(cx, op, g);
+    }
+}
+
+// Replica of a split-side vector for the other side's gathers: the owned slice
+// is copied into its place of `rep` (world * L) and all-gathered in place.
+static void refresh(Ctx& cx, int side, VecSel src, double* rep, Gate g)
+{
+    const cpd_problem* P = cx.P;
+    if (P->split != side) return;
+    const int64_t N = P->own_len[side];
+    const int gr = (int)std::max<int64_t>(1, std::min<int64_t>((N + TPB - 1) / TPB, cx.grid_elem));
+    g.active = nullptr;
+    k_copy_sel<<<gr, TPB, 0, cx.st>>>(N, rep + (int64_t)P->rank * P->L, src, g, cx.ctl);
+    CPD_CUDA(cudaGetLastError());
+    ++cx.launches;
+    cx.all_gather_inplace(rep, P->L);
 }
 
 static Gate always() { return Gate{GATE_ALWAYS, 0, 0, nullptr}; }
 static VecSel fixed(const double* v) { return VecSel{v, v, 0}; }
 static VecSel none() { return VecSel{nullptr, nullptr, 0}; }
 
+// Replica of the split side for one-off evaluations: `ext` (world * L doubles)
+// or a scratch allocation.
+struct Reps {
+    DBuf<double> own;
+    double* r = nullptr;
+    explicit Reps(const cpd_problem* P, double* ext = nullptr)
+    {
+        if (P->split < 0) return;
+        if (ext) {
+            r = ext;
+            return;
+        }
+        own.alloc((size_t)P->world * P->L);
+        CPD_CUDA(cudaMemset(own.p, 0, sizeof(double) * P->world * P->L));
+        r = own.p;
+    }
+    // gathered view of an owned vector of `side` (refreshing the replica if split)
+    const double* view(Ctx& cx, int side, const double* v)
+    {
+        if (cx.P->split != side) return v;
+        refresh(cx, side, fixed(v), r, always());
+        return r;
+    }
+};
+
 // Standalone evaluations shared by the solver and the stand-alone ABI calls.
-// score of (x, y) for objective c / bounds bd -> cx.h_ctl->last (after pull)
+// score of (x, y) (owned parts) for objective c / bounds bd (owned parts)
 static void eval_score(Ctx& cx, const double* x, const double* y, const double* c, Bounds bd,
                        double nb, double nc, double out[8])
 {
     AuxScope aux(cx);
     const cpd_problem* P = cx.P;
+    Reps rp(P);
     Ctl h{};
     h.nb = nb;
     h.nc = nc;
     h.K = 1;
     cx.push_ctl(h);
-    EpiInitM em{P->b.p, y, nullptr};
-    launch_spmv<1>(cx, P->A, cx.planA(), fixed(x), none(), em, always());
+    EpiInitM em{P->b_own(), y, nullptr};
+    pass<1>(cx, 0, fixed(rp.view(cx, 1, x)), none(), em, always());
     EpiInitN en{c, x, bd, 0};
-    launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(y), none(), en, always());
+    pass<1>(cx, 1, fixed(rp.view(cx, 0, y)), none(), en, always());
     cx.pull_ctl();
     for (int i = 0; i < 8; ++i) out[i] = cx.h_ctl->last[i];
 }
@@ -173,8 +285,8 @@ static void eval_norms(Ctx& cx, const double* b, const double* c, double* nb, do
     h.mode = MODE_NONE;
     h.eta = 1.0;
     cx.push_ctl(h);
-    OpNorms on{b, c, P->n, P->m, 1.0};
-    launch_elem(cx, std::max<int64_t>(P->n, P->m), on, always());
+    OpNorms on{b, c, P->own_len[1], P->own_len[0], 1.0};
+    elem(cx, std::max(P->own_len[1], P->own_len[0]), on, always(), true);
     cx.pull_ctl();
     *nb = cx.h_ctl->nb;
     *nc = cx.h_ctl->nc;
@@ -188,8 +300,8 @@ static void eval_stats(Ctx& cx, const double* x, const double* z, const double* 
     Ctl h{};
     h.K = 1;
     cx.push_ctl(h);
-    OpStats os{x, z, lh, uh, P->bounds(), eps};
-    launch_elem(cx, P->n, os, always());
+    OpStats os{x, z, lh, uh, P->bounds_own(), eps};
+    elem(cx, P->own_len[1], os, always(), true);
     cx.pull_ctl();
     const double* o = cx.h_ctl->out;
     std::memset(out, 0, sizeof(*out));
@@ -200,30 +312,37 @@ static void eval_stats(Ctx& cx, const double* x, const double* z, const double* 
     out->candidates = z ? (int64_t)o[4] : 0;
     out->fix_lb = fix_lb;
     out->fix_ub = fix_ub;
-    const int64_t m = P->m;
+    const int64_t m = P->m_glob;
     out->est_primal_pushes = std::max<int64_t>(out->off_bound - m, 0);
     out->est_dual_pushes = z ? std::max<int64_t>(m - out->zero_rc, 0) : 0;
     const int64_t thr = std::max<int64_t>(2 * m, floor_);
     out->is_candidate = z ? (out->candidates >= thr) : 0;
 }
 
+// sigma_hat by `iters` power iterations; v (n-side owned), w (m-side owned) scratch.
+static void power_iterate(Ctx& cx, Reps& rp, int32_t iters, uint64_t seed, double* v, double* w)
+{
+    const cpd_problem* P = cx.P;
+    OpPowInit pi{v, seed, P->own_len[1], P->gofs[1]};
+    elem(cx, P->own_len[1], pi, always(), true);
+    for (int it = 0; it < iters; ++it) {
+        EpiPowM pm{w, 0.0};
+        pass<1>(cx, 0, fixed(rp.view(cx, 1, v)), none(), pm, always());
+        EpiPowN pn{v};
+        pass<1>(cx, 1, fixed(rp.view(cx, 0, w)), none(), pn, always());
+    }
+}
+
 static double power_sigma(Ctx& cx, int32_t iters, uint64_t seed, double step_scale, double* v,
                           double* w)
 {
     AuxScope aux(cx);
-    const cpd_problem* P = cx.P;
+    Reps rp(cx.P);
     Ctl h{};
     h.K = 1;
     h.step_scale = step_scale;
     cx.push_ctl(h);
-    OpPowInit pi{v, seed, P->n};
-    launch_elem(cx, P->n, pi, always());
-    for (int it = 0; it < iters; ++it) {
-        EpiPowM pm{w, 0.0};
-        launch_spmv<1>(cx, P->A, cx.planA(), fixed(v), none(), pm, always());
-        EpiPowN pn{v};
-        launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(w), none(), pn, always());
-    }
+    power_iterate(cx, rp, iters, seed, v, w);
     cx.pull_ctl();
     return cx.h_ctl->sigma_hat;
 }
@@ -286,7 +405,10 @@ struct cpd_solver {
     const cpd_problem* P;
     cpd_params prm;
     Ctx cx;
+    // state vectors: n-side (x-like) of length own_len[1], m-side (y-like) own_len[0]
     DBuf<double> X0, X1, Xa0, Xa1, Xr, Y, Ya, Yr, AX, AXa, Ystar, Z, lhat, uhat, chat, objd, SN, SM;
+    // replicas of the split side (world * L): current vector / its average
+    DBuf<double> RV, RA;
     DBuf<int64_t> trk, troff;
     DBuf<double> trrp;
     DBuf<int32_t> active;
@@ -312,11 +434,18 @@ struct cpd_solver {
 
     cpd_solver(const cpd_problem* p, const cpd_params& pr) : P(p), prm(pr), cx(p)
     {
-        const size_t n = p->n, m = p->m;
+        const size_t n = p->own_len[1], m = p->own_len[0];
         for (auto* b : {&X0, &X1, &Xa0, &Xa1, &Xr, &Z, &lhat, &uhat, &chat, &objd, &SN}) b->alloc(n);
         for (auto* b : {&Y, &Ya, &Yr, &AX, &AXa, &Ystar, &SM}) b->alloc(m);
         for (auto* b : {&X0, &X1, &Xa0, &Xa1, &Xr, &Z}) CPD_CUDA(cudaMemset(b->p, 0, sizeof(double) * n));
         for (auto* b : {&Y, &Ya, &Yr, &AX, &AXa, &Ystar}) CPD_CUDA(cudaMemset(b->p, 0, sizeof(double) * m));
+        if (p->split >= 0) {
+            const size_t R = (size_t)p->world * p->L;
+            RV.alloc(R);
+            RA.alloc(R);
+            CPD_CUDA(cudaMemset(RV.p, 0, sizeof(double) * R));
+            CPD_CUDA(cudaMemset(RA.p, 0, sizeof(double) * R));
+        }
         trk.alloc(traj_cap);
         troff.alloc(traj_cap);
         trrp.alloc(traj_cap);
@@ -343,18 +472,22 @@ struct cpd_solver {
         for (auto e : ev1) cudaEventDestroy(e);
         if (h_active) cudaFreeHost(h_active);
     }
+    int32_t nO() const { return P->own_len[1]; }
+    int32_t mO() const { return P->own_len[0]; }
     double* Xp(int par) { return par ? X1.p : X0.p; }
 
-    const double* obj_of(int kind) const { return kind ? chat.p : P->c.p; }
+    const double* obj_of(int kind) const { return kind ? chat.p : P->c_own(); }
     Bounds bounds_of(int kind) const
     {
-        return kind ? Bounds{lhat.p, uhat.p, 0.0, 0.0} : P->bounds();
+        return kind ? Bounds{lhat.p, uhat.p, 0.0, 0.0} : P->bounds_own();
     }
+    // gather source of an owned vector of `side`: the replica when that side is split
+    VecSel gsrc(int side, VecSel own, double* rep) const { return P->split == side ? fixed(rep) : own; }
 
     // ---------------------------------------------------------- begin
     void begin(const RunCfg& rc)
     {
-        const int32_t n = P->n, m = P->m;
+        const int32_t n = nO(), m = mO();
         Ctl h{};
         h.mode = rc.mode;
         h.restart_on = prm.restart ? 1 : 0;
@@ -378,27 +511,20 @@ struct cpd_solver {
         h.traj_off = troff.p;
         h.traj_rp = trrp.p;
         cx.push_ctl(h);
-        if (rc.power) {
-            // power iteration into scratch (SN, SM); writes ctl->eta
-            OpPowInit pi{SN.p, prm.seed, n};
-            launch_elem(cx, n, pi, always());
-            for (int it = 0; it < prm.power_iters; ++it) {
-                EpiPowM pm{SM.p, 0.0};
-                launch_spmv<1>(cx, P->A, cx.planA(), fixed(SN.p), none(), pm, always());
-                EpiPowN pn{SN.p};
-                launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(SM.p), none(), pn, always());
-            }
-        }
+        Reps rp(P, RV.p);
+        if (rc.power) power_iterate(cx, rp, prm.power_iters, prm.seed, SN.p, SM.p);   // writes ctl->eta
         const double* c = obj_of(rc.kind);
         const Bounds bd = bounds_of(rc.kind);
-        OpNorms on{P->b.p, c, n, m, rc.omega_in};
-        launch_elem(cx, std::max(n, m), on, always());
+        OpNorms on{P->b_own(), c, n, m, rc.omega_in};
+        elem(cx, std::max(n, m), on, always(), true);
         OpBegin ob{rc.xs, rc.ys, bd, X0.p, Xa0.p, Xa1.p, Xr.p, Y.p, Ya.p, Yr.p, n, m, rc.ys ? 0 : 1};
-        launch_elem(cx, std::max(n, m), ob, always());
-        EpiInitM em{P->b.p, Y.p, AX.p};
-        launch_spmv<1>(cx, P->A, cx.planA(), fixed(X0.p), none(), em, always());
+        elem(cx, std::max(n, m), ob, always(), false);
+        EpiInitM em{P->b_own(), Y.p, AX.p};
+        pass<1>(cx, 0, fixed(rp.view(cx, 1, X0.p)), none(), em, always());
         EpiInitN en{c, X0.p, bd, 1};
-        launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), en, always());
+        // the batch's K1 gathers the y replica: refresh it here (split m-side)
+        refresh(cx, 0, fixed(Y.p), RV.p, always());
+        pass<1>(cx, 1, gsrc(0, fixed(Y.p), RV.p), none(), en, always());
         cx.pull_ctl();
         cur_par = 0;
         run_active = true;
@@ -411,11 +537,11 @@ struct cpd_solver {
     void enqueue_batch(int kind, bool capture)
     {
         const int64_t l0 = cx.launches;
-        const int32_t n = P->n, m = P->m;
+        const int32_t n = nO(), m = mO();
         const int K = prm.check_every;
         const double* c = obj_of(kind);
         const Bounds bd = bounds_of(kind);
-        const Bounds orig = P->bounds();
+        const Bounds orig = P->bounds_own();
         const PingPong X{{X0.p, X1.p}}, Xa{{Xa0.p, Xa1.p}};
         auto rec = [&](std::vector<cudaEvent_t>& ev, int node) {
             if (!prm.profile) return;
@@ -428,37 +554,48 @@ struct cpd_solver {
             EpiCheckN e{c, bd, orig, X, Xa, Xr.p, prm.restart ? 1 : 0, 0.0, nullptr, nullptr, 0};
             Gate g{GATE_CHECK, 0, NODE_CHECK_N, active.p};
             rec(ev0, NODE_CHECK_N);
-            if (prm.restart)
-                launch_spmv<2>(cx, P->AT, cx.planAT(), fixed(Y.p), fixed(Ya.p), e, g);
-            else
-                launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), e, g);
+            // RV holds y_k (refreshed after every dual step); RA <- average of y
+            if (prm.restart) {
+                refresh(cx, 0, fixed(Ya.p), RA.p, g);
+                pass<2>(cx, 1, gsrc(0, fixed(Y.p), RV.p), gsrc(0, fixed(Ya.p), RA.p), e, g);
+            } else {
+                pass<1>(cx, 1, gsrc(0, fixed(Y.p), RV.p), none(), e, g);
+            }
             rec(ev1, NODE_CHECK_N);
-            EpiCheckM em{P->b.p, Y.p, Ya.p, Yr.p, AXa.p};
+            EpiCheckM em{P->b_own(), Y.p, Ya.p, Yr.p, AXa.p};
             Gate gm{GATE_CHECK, 0, NODE_CHECK_M, active.p};
             rec(ev0, NODE_CHECK_M);
-            launch_spmv<1>(cx, P->A, cx.planA(), VecSel{Xa0.p, Xa1.p, 2}, none(), em, gm);
+            refresh(cx, 1, VecSel{Xa0.p, Xa1.p, 2}, RA.p, gm);
+            pass<1>(cx, 0, gsrc(1, VecSel{Xa0.p, Xa1.p, 2}, RA.p), none(), em, gm);
             rec(ev1, NODE_CHECK_M);
             OpRestart orr{X, Xa, Y.p, Ya.p, AX.p, AXa.p, Xr.p, Yr.p, n, m, 0, nullptr, nullptr};
             Gate gr{GATE_RESTART, 0, NODE_RESTART, active.p};
             rec(ev0, NODE_RESTART);
-            launch_elem(cx, std::max(n, m), orr, gr);
+            elem(cx, std::max(n, m), orr, gr, false);
+            refresh(cx, 0, fixed(Y.p), RV.p, gr);   // y may have changed
             rec(ev1, NODE_RESTART);
         }
         for (int s = 0; s < K; ++s) {
             const int n1 = NODE_K0 + 2 * s, n2 = n1 + 1;
+            const Gate g1{GATE_K1, s, n1, active.p}, g2{GATE_K2, s, n2, active.p};
             rec(ev0, n1);
+            const VecSel ysrc = gsrc(0, fixed(Y.p), RV.p);
             if (kind == 0 && P->uniform_bounds) {   // scalar bounds: 3 staged per-row inputs
                 EpiPrimalT<false> e1{c, bd, X, Xa, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr};
-                launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), e1, Gate{GATE_K1, s, n1, active.p});
+                pass<1>(cx, 1, ysrc, none(), e1, g1);
             } else {
                 EpiPrimalT<true> e1{c, bd, X, Xa, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr};
-                launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), e1, Gate{GATE_K1, s, n1, active.p});
+                pass<1>(cx, 1, ysrc, none(), e1, g1);
             }
+            // x_{k+1} replica for the dual step's gathers (split n-side); the
+            // gate is the dual step's: it runs exactly when the dual step does
+            refresh(cx, 1, VecSel{X0.p, X1.p, 1}, RV.p, g2);
             rec(ev1, n1);
-            EpiDual e2{P->b.p, Y.p, Ya.p, AX.p, 0.0, 0.0};
+            EpiDual e2{P->b_own(), Y.p, Ya.p, AX.p, 0.0, 0.0};
             rec(ev0, n2);
-            launch_spmv<1>(cx, P->A, cx.planA(), VecSel{X0.p, X1.p, 1}, none(), e2,
-                           Gate{GATE_K2, s, n2, active.p});
+            pass<1>(cx, 0, gsrc(1, VecSel{X0.p, X1.p, 1}, RV.p), none(), e2, g2);
+            // y_{k+1} replica for the next primal step (split m-side); k already advanced
+            refresh(cx, 0, fixed(Y.p), RV.p, always());
             rec(ev1, n2);
         }
         if (capture) graph_kernels[kind] = cx.launches - l0;
@@ -522,7 +659,8 @@ struct cpd_solver {
             if (h.k >= k_stop && !h.check_pending) break;
             run_batch();
             if (time_limit > 0.0 && !cx.h_ctl->done) {
-                const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                cx.allreduce_max_host(&el);   // distributed: one decision for all ranks
                 if (el > time_limit) {
                     cx.set_i32(&cx.ctl->status, ST_TIME_LIMIT);
                     cx.set_i64(&cx.ctl->iterations, cx.h_ctl->k);
@@ -542,9 +680,9 @@ struct cpd_solver {
         const int64_t k = h.k;
         cur_par = (int)(k & 1);
         if (h.returned_average) {
-            const int g = std::min<int64_t>(cx.grid_elem, ((int64_t)std::max(P->n, P->m) + 255) / 256);
-            k_copy<<<g, 256, 0, cx.st>>>(P->n, Xp(cur_par), (k & 1) ? Xa1.p : Xa0.p);
-            k_copy<<<g, 256, 0, cx.st>>>(P->m, Y.p, Ya.p);
+            const int g = std::min<int64_t>(cx.grid_elem, ((int64_t)std::max(nO(), mO()) + 255) / 256 + 1);
+            k_copy<<<g, 256, 0, cx.st>>>(nO(), Xp(cur_par), (k & 1) ? Xa1.p : Xa0.p);
+            k_copy<<<g, 256, 0, cx.st>>>(mO(), Y.p, Ya.p);
             CPD_CUDA(cudaGetLastError());
             cx.launches += 2;
         }
@@ -615,29 +753,32 @@ struct cpd_solver {
     {
         const auto t0 = std::chrono::steady_clock::now();
         if (run_active) commit();
-        const int32_t n = P->n, m = P->m;
+        const int32_t n = nO(), m = mO();
         corner_eps = cp.eps_abs;
-        const int g = std::min<int64_t>(cx.grid_elem, ((int64_t)std::max(n, m) + 255) / 256);
+        const int g = std::min<int64_t>(cx.grid_elem, ((int64_t)std::max(n, m) + 255) / 256 + 1);
         // phase-1 solution (x*, y*): x* stays in X[cur_par]; y* saved in Ystar
         k_copy<<<g, 256, 0, cx.st>>>(m, Ystar.p, Y.p);
         CPD_CUDA(cudaGetLastError());
         ++cx.launches;
         const double* obj = nullptr;
         if (cp.obj) {
-            CPD_CUDA(cudaMemcpyAsync(objd.p, cp.obj, sizeof(double) * n,
-                                     cp.obj_mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                     cx.st));
+            if (n > 0)
+                CPD_CUDA(cudaMemcpyAsync(objd.p, cp.obj + P->gofs[1], sizeof(double) * n,
+                                         cp.obj_mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                  : cudaMemcpyHostToDevice,
+                                         cx.st));
             obj = objd.p;
         }
         // Algorithm 1 line 2: z*, bound map, objective
         {
             AuxScope aux(cx);
+            Reps rp(P, RV.p);
             Ctl h{};
             h.K = 1;
             cx.push_ctl(h);
-            EpiCorner ec{P->c.p, Xp(cur_par), P->bounds(), Z.p, lhat.p, uhat.p, chat.p, obj, cp.eps_abs,
-                         cp.obj_scale, cp.seed};
-            launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Ystar.p), none(), ec, always());
+            EpiCorner ec{P->c_own(), Xp(cur_par), P->bounds_own(), Z.p, lhat.p, uhat.p, chat.p, obj, cp.eps_abs,
+                         cp.obj_scale, cp.seed, P->gofs[1]};
+            pass<1>(cx, 1, fixed(rp.view(cx, 0, Ystar.p)), none(), ec, always());
             cx.pull_ctl();
             fix_lb = (int64_t)cx.h_ctl->out[0];
             fix_ub = (int64_t)cx.h_ctl->out[1];
@@ -678,13 +819,18 @@ struct cpd_solver {
                        after);
     }
 
+    // x: n-side vector, y: m-side vector, both GLOBAL length; each rank takes its part.
     void set_iterate(const double* x, const double* y, int mem)
     {
         const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-        if (x) CPD_CUDA(cudaMemcpyAsync(X0.p, x, sizeof(double) * P->n, kind, cx.st));
-        else CPD_CUDA(cudaMemsetAsync(X0.p, 0, sizeof(double) * P->n, cx.st));
-        if (y) CPD_CUDA(cudaMemcpyAsync(Y.p, y, sizeof(double) * P->m, kind, cx.st));
-        else CPD_CUDA(cudaMemsetAsync(Y.p, 0, sizeof(double) * P->m, cx.st));
+        if (nO() > 0) {
+            if (x) CPD_CUDA(cudaMemcpyAsync(X0.p, x + P->gofs[1], sizeof(double) * nO(), kind, cx.st));
+            else CPD_CUDA(cudaMemsetAsync(X0.p, 0, sizeof(double) * nO(), cx.st));
+        }
+        if (mO() > 0) {
+            if (y) CPD_CUDA(cudaMemcpyAsync(Y.p, y + P->gofs[0], sizeof(double) * mO(), kind, cx.st));
+            else CPD_CUDA(cudaMemsetAsync(Y.p, 0, sizeof(double) * mO(), cx.st));
+        }
         cx.sync();
         cur_par = 0;
         run_active = false;
@@ -695,40 +841,62 @@ struct cpd_solver {
     void compute_z()
     {
         AuxScope aux(cx);
+        Reps rp(P, RV.p);
         Ctl h{};
         h.K = 1;
         cx.push_ctl(h);
-        EpiZ ez{P->c.p, Z.p};
-        launch_spmv<1>(cx, P->AT, cx.planAT(), fixed(Y.p), none(), ez, always());
+        EpiZ ez{P->c_own(), Z.p};
+        pass<1>(cx, 1, fixed(rp.view(cx, 0, Y.p)), none(), ez, always());
+        cx.sync();
+    }
+
+    // Full (global) vector of `side` from every rank's owned part.
+    void gather_full(int side, const double* own, double* out, int mem)
+    {
+        const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        if (P->world == 1 && P->split < 0) {
+            CPD_CUDA(cudaMemcpyAsync(out, own, sizeof(double) * P->own_len[side], kind, cx.st));
+            return;
+        }
+        int64_t Lmax = 1;
+        for (int64_t l : P->rank_len[side]) Lmax = std::max(Lmax, l);
+        DBuf<double> send(Lmax), all((size_t)Lmax * P->world);
+        if (P->own_len[side] > 0)
+            CPD_CUDA(cudaMemcpyAsync(send.p, own, sizeof(double) * P->own_len[side], cudaMemcpyDeviceToDevice,
+                                     cx.st));
+        cx.all_gather(send.p, all.p, Lmax);
+        for (int q = 0; q < P->world; ++q)
+            if (P->rank_len[side][q] > 0)
+                CPD_CUDA(cudaMemcpyAsync(out + P->rank_gofs[side][q], all.p + (int64_t)q * Lmax,
+                                         sizeof(double) * P->rank_len[side][q], kind, cx.st));
         cx.sync();
     }
 
     void get_iterate(double* x, double* y, double* z, int mem)
     {
-        const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
         if (z) compute_z();
-        if (x) CPD_CUDA(cudaMemcpyAsync(x, Xp(cur_par), sizeof(double) * P->n, kind, cx.st));
-        if (y) CPD_CUDA(cudaMemcpyAsync(y, Y.p, sizeof(double) * P->m, kind, cx.st));
-        if (z) CPD_CUDA(cudaMemcpyAsync(z, Z.p, sizeof(double) * P->n, kind, cx.st));
+        if (x) gather_full(1, Xp(cur_par), x, mem);
+        if (y) gather_full(0, Y.p, y, mem);
+        if (z) gather_full(1, Z.p, z, mem);
         cx.sync();
     }
 
     double kernel_bytes(const std::string& name) const
     {
-        const double nnz = (double)P->nnz, n = P->n, m = P->m;
+        // local (this rank's) algorithmic bytes: matrix block + owned vectors + gathered vector
+        const double nnz = (double)P->nnz, nr = P->n, mr = P->m, n = nO(), m = mO();
         const bool corner = name.find(":corner") != std::string::npos;
         const std::string base = name.substr(0, name.find(':'));
         const double bnd = (corner || !P->uniform_bounds) ? 16.0 * n : 0.0;
-        if (base == "primal_step_AT") return 12 * nnz + 4 * (n + 1) + 8 * m + 40 * n + bnd;
-        if (base == "dual_step_A") return 12 * nnz + 4 * (m + 1) + 8 * n + 56 * m;
+        if (base == "primal_step_AT") return 12 * nnz + 4 * (nr + 1) + 8 * mr + 40 * n + bnd;
+        if (base == "dual_step_A") return 12 * nnz + 4 * (mr + 1) + 8 * nr + 56 * m;
         if (base == "check_eval_AT")
-            return 12 * nnz + 4 * (n + 1) + (prm.restart ? 16 : 8) * m + 32 * n + bnd + (corner ? 16 * n : 0);
-        if (base == "check_eval_A") return 12 * nnz + 4 * (m + 1) + 8 * n + 40 * m;
+            return 12 * nnz + 4 * (nr + 1) + (prm.restart ? 16 : 8) * mr + 32 * n + bnd + (corner ? 16 * n : 0);
+        if (base == "check_eval_A") return 12 * nnz + 4 * (mr + 1) + 8 * nr + 40 * m;
         if (base == "restart_apply") return 32 * n + 48 * m;
         return -1.0;
     }
 };
-
 // ====================================================================== ABI
 static thread_local std::string g_err;
 
@@ -753,9 +921,43 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
                                      const double* c, const double* lb, const double* ub,
                                      int32_t mem, int32_t device);
 
+cpd_problem* cpd_problem_create_dist_impl(int32_t rank, int32_t world, const char id[128], int32_t partition,
+                                          int32_t m, int32_t n, int64_t nnz, const int32_t* ATp,
+                                          const int32_t* ATj, const double* ATx, const double* b,
+                                          const double* c, const double* lb, const double* ub, int32_t device);
+
 extern "C" {
 
 const char* cpd_last_error(void) { return g_err.c_str(); }
+
+int cpd_problem_create_dist(int32_t rank, int32_t world, const char id[128], int32_t partition, int32_t m,
+                            int32_t n, int64_t nnz, const int32_t* AT_rowptr, const int32_t* AT_col,
+                            const double* AT_val, const double* b, const double* c, const double* lb,
+                            const double* ub, int32_t device, cpd_problem** out)
+{
+    ABI_BEGIN
+    if (!out) return fail(CPD_E_ARG, "out is NULL");
+    *out = cpd_problem_create_dist_impl(rank, world, id, partition, m, n, nnz, AT_rowptr, AT_col, AT_val, b, c,
+                                        lb, ub, device);
+    ABI_END
+}
+
+int cpd_problem_dist_info(const cpd_problem* p, int64_t info[10])
+{
+    ABI_BEGIN
+    if (!p || !info) return fail(CPD_E_ARG, "NULL argument");
+    info[0] = p->world;
+    info[1] = p->rank;
+    info[2] = p->split < 0 ? -1 : (p->split == 1 ? 0 : 1);   // partition
+    info[3] = p->L;
+    info[4] = p->own_len[0];
+    info[5] = p->own_len[1];
+    info[6] = p->gofs[0];
+    info[7] = p->gofs[1];
+    info[8] = p->m;
+    info[9] = p->n;
+    ABI_END
+}
 int cpd_version(void) { return CPD_VERSION; }
 
 int cpd_problem_create(int32_t m, int32_t n, int64_t nnz, const int32_t* A_rowptr, const int32_t* A_col,
@@ -784,8 +986,8 @@ int cpd_problem_info(const cpd_problem* p, int64_t info[8])
 {
     ABI_BEGIN
     if (!p || !info) return fail(CPD_E_ARG, "NULL argument");
-    info[0] = p->m;
-    info[1] = p->n;
+    info[0] = p->m_glob;
+    info[1] = p->n_glob;
     info[2] = p->nnz;
     info[3] = p->A.plan.nlong;
     info[4] = p->AT.plan.nlong;
@@ -947,7 +1149,7 @@ int cpd_power_sigma(const cpd_problem* p, int32_t iters, uint64_t seed, double* 
     if (!p || !sigma || iters < 1) return fail(CPD_E_ARG, "bad argument");
     CPD_CUDA(cudaSetDevice(p->device));
     Ctx cx(p);
-    DBuf<double> v(p->n), w(p->m);
+    DBuf<double> v(std::max(p->own_len[1], 1)), w(std::max(p->own_len[0], 1));
     *sigma = power_sigma(cx, iters, seed, 1.0, v.p, w.p);
     ABI_END
 }
@@ -958,19 +1160,15 @@ int cpd_problem_score(const cpd_problem* p, const double* x, const double* y, in
     if (!p || !x || !y || !out) return fail(CPD_E_ARG, "NULL argument");
     CPD_CUDA(cudaSetDevice(p->device));
     Ctx cx(p);
-    DBuf<double> dx, dy;
-    const double *px = x, *py = y;
-    if (mem != CPD_DEVICE) {
-        dx.alloc(p->n);
-        dy.alloc(p->m);
-        CPD_CUDA(cudaMemcpy(dx.p, x, sizeof(double) * p->n, cudaMemcpyHostToDevice));
-        CPD_CUDA(cudaMemcpy(dy.p, y, sizeof(double) * p->m, cudaMemcpyHostToDevice));
-        px = dx.p;
-        py = dy.p;
-    }
+    // owned parts of the (global) x and y
+    const int64_t nO = p->own_len[1], mO = p->own_len[0];
+    DBuf<double> dx(std::max<int64_t>(nO, 1)), dy(std::max<int64_t>(mO, 1));
+    const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (nO) CPD_CUDA(cudaMemcpy(dx.p, x + p->gofs[1], sizeof(double) * nO, kind));
+    if (mO) CPD_CUDA(cudaMemcpy(dy.p, y + p->gofs[0], sizeof(double) * mO, kind));
     double nb, nc;
-    eval_norms(cx, p->b.p, p->c.p, &nb, &nc);
-    eval_score(cx, px, py, p->c.p, p->bounds(), nb, nc, out);
+    eval_norms(cx, p->b_own(), p->c_own(), &nb, &nc);
+    eval_score(cx, dx.p, dy.p, p->c_own(), p->bounds_own(), nb, nc, out);
     ABI_END
 }
 
@@ -982,16 +1180,18 @@ int cpd_compute_stats(const cpd_problem* p, const double* x, const double* z, co
     if (!p || !x || !out || ((lhat == nullptr) != (uhat == nullptr))) return fail(CPD_E_ARG, "bad argument");
     CPD_CUDA(cudaSetDevice(p->device));
     Ctx cx(p);
+    // owned parts of the (global) n-vectors
     DBuf<double> b[4];
     const double* src[4] = {x, z, lhat, uhat};
-    const double* dev[4] = {x, z, lhat, uhat};
-    if (mem != CPD_DEVICE)
-        for (int i = 0; i < 4; ++i)
-            if (src[i]) {
-                b[i].alloc(p->n);
-                CPD_CUDA(cudaMemcpy(b[i].p, src[i], sizeof(double) * p->n, cudaMemcpyHostToDevice));
-                dev[i] = b[i].p;
-            }
+    const double* dev[4] = {nullptr, nullptr, nullptr, nullptr};
+    const int64_t nO = p->own_len[1];
+    const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (int i = 0; i < 4; ++i)
+        if (src[i]) {
+            b[i].alloc(std::max<int64_t>(nO, 1));
+            if (nO) CPD_CUDA(cudaMemcpy(b[i].p, src[i] + p->gofs[1], sizeof(double) * nO, kind));
+            dev[i] = b[i].p;
+        }
     eval_stats(cx, dev[0], dev[1], dev[2], dev[3], eps_abs, candidate_floor, 0, 0, out);
     ABI_END
 }

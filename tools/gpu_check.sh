@@ -15,6 +15,6 @@ tail -c 3000 $OUT/bench.json
 if [ "${NCU:-1}" = "1" ]; then
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
      python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --tte '' > $OUT/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-  timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:EpiPrimal|EpiDual" -s 3 -c 6 \
+  timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:EpiPrimal|EpiDual" -s 3 -c 6 \
      -o $OUT/full python tools/prof_run.py --iters 4 > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi
