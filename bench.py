@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tte", default="c2,c4", help="configs for the time-to-eps side measurement ('' = off)")
     ap.add_argument("--ref-iters", type=int, default=0, help="oracle iterations per reference step (0: auto)")
+    ap.add_argument("--partition", type=int, default=-1,
+                    help="multi-GPU partition: 0 row-block, 1 col-block, -1 auto (shard the long side)")
     return ap.parse_args()
 
 
@@ -143,6 +145,22 @@ def dist_init(n):
         torch.cuda.set_device(local)
     dist.init_process_group(backend)
     return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def run_step(S, iters1, iters2):
@@ -247,16 +265,25 @@ def main():
     import paper_2511_13894_b200 as cpd
     dev = local
     torch.cuda.set_device(dev)
+    uid = None
     if world > 1:
-        raise SystemExit("multi-GPU bench: see DESIGN.md (row-block path)")
+        import torch.distributed as dist
+        obj = [cpd.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
     # resident problem (a0: validation + transpose + plans happen here, untimed)
-    P = cpd.Problem.from_lp(lp, device=dev)
+    if world > 1:
+        P = cpd.Problem.create_dist(lp, rank, world, uid, partition=args.partition, device=dev)
+    else:
+        P = cpd.Problem.from_lp(lp, device=dev)
     S = cpd.Solver(P, max_iters=args.iters1, profile=1)
+    P_info = P.dist_info()
     for _ in range(args.warmup):
         run_step(S, args.iters1, args.iters2)
     S.kernel_times(reset=True)
     c0 = S.counters()["launches"]
     torch.cuda.synchronize()
+    barrier(world)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     iters = 0
     last = None
@@ -268,7 +295,8 @@ def main():
             last = (r1, r2, before, after)
         ev1.record()
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    barrier(world)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
     launches = S.counters()["launches"] - c0
     value = iters / (ms / 1e3)
     kt = S.kernel_times()
@@ -302,23 +330,29 @@ def main():
         "corner_stats": {"before": before, "after": after},
     }
     with_e2e = not args.no_e2e
+    S.close()
+    P.close()
     if with_e2e:
-        res["e2e"] = e2e_measure(args, lp, dev)
+        res["e2e"] = e2e_measure(args, lp, dev, rank, world)
     clk_s = clk.summary()
     res["clocks"] = clk_s
-    if args.tte:
+    if world > 1:
+        res["partition"] = {0: "row-block", 1: "col-block"}[P_info["partition"]]
+    if args.tte and world == 1:
         try:
             res["time_to_eps"] = time_to_eps([x for x in args.tte.split(",") if x], dev)
         except Exception as e:  # pragma: no cover
             res["time_to_eps"] = {"error": str(e)}
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         res["cpu_baseline"] = cpu_baseline(lp)
-    print(json.dumps(res), flush=True)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
 
 
-def e2e_measure(args, lp, dev):
+def e2e_measure(args, lp, dev, rank=0, world=1):
     """Public API with HOST buffers: H2D of the LP from pinned memory, problem
-    creation (device validation + transpose), solve + corner push, D2H of x, y, z."""
+    creation (device validation + transpose), solve + corner push, D2H of x, y, z.
+    N > 1: every rank creates its block from the same host arrays (collective)."""
     import torch
     import paper_2511_13894_b200 as cpd
     pin = {}
@@ -334,9 +368,21 @@ def e2e_measure(args, lp, dev):
     d2h = xo.nbytes + yo.nbytes + zo.nbytes
     steps = args.e2e_steps or max(1, min(args.steps, 2))
 
+    uid = None
+    if world > 1:
+        import torch.distributed as dist
+
     def one():
-        P = cpd.Problem(lp.m, lp.n, AT=(pin["ATp"], pin["ATj"], pin["ATx"]), b=pin["b"], c=pin["c"],
-                        lb=pin["lb"], ub=pin["ub"], device=dev)
+        if world > 1:
+            obj = [cpd.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            import types
+            hl = types.SimpleNamespace(m=lp.m, n=lp.n, ATp=pin["ATp"], ATj=pin["ATj"], ATx=pin["ATx"], b=pin["b"],
+                                       c=pin["c"], lb=pin["lb"], ub=pin["ub"])
+            P = cpd.Problem.create_dist(hl, rank, world, obj[0], partition=args.partition, device=dev)
+        else:
+            P = cpd.Problem(lp.m, lp.n, AT=(pin["ATp"], pin["ATj"], pin["ATx"]), b=pin["b"], c=pin["c"],
+                            lb=pin["lb"], ub=pin["ub"], device=dev)
         S = cpd.Solver(P, max_iters=args.iters1)
         r1 = S.solve()
         r2, _, _ = S.corner_push(max_iters=args.iters2, candidate_floor=100_000)
@@ -348,12 +394,13 @@ def e2e_measure(args, lp, dev):
 
     one()   # warm-up
     torch.cuda.synchronize()
+    barrier(world)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     iters = sum(one() for _ in range(steps))
     ev1.record()
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
     return {"value": iters / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "steps": steps, "ms_per_step": ms / steps}
 

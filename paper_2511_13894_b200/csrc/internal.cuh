@@ -73,13 +73,29 @@ struct Plan {
 void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rowptr, const int32_t* d_p,
                 const int32_t* d_col, Plan& plan);
 
+// SELL-32 copy of a CSR layout whose rows are short and of similar length
+// (DESIGN.md §6): slices of 32 consecutive rows, each padded to its longest row,
+// stored column-major inside the slice so lane = row reads coalesced.
+struct Sell {
+    DBuf<int64_t> sp;      // [nslice + 1] slice starts (padded entries)
+    DBuf<int32_t> col;     // -1 = padding
+    DBuf<double> val;
+    int32_t nslice = 0;
+    int64_t padded = 0;
+    bool on = false;
+};
+
 struct Matrix {
     DBuf<int32_t> p, j;
     DBuf<double> x;
     int32_t rows = 0, cols = 0;
     Plan plan;
+    Sell sell;
     DevCsr dev() const { return DevCsr{p.p, j.p, x.p, rows}; }
+    DevSell dsell() const { return DevSell{sell.sp.p, sell.col.p, sell.val.p, rows, sell.nslice}; }
 };
+// Build M.sell when the padded size is at most `max_ratio` x nnz (else M.sell.on = false).
+void build_sell(Matrix& M, int64_t nnz, double max_ratio);
 
 }  // namespace cpd
 

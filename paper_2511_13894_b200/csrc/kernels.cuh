@@ -704,6 +704,90 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
     grid_finalize<NS>(acc, bpart, ctr, prev, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
 }
 
+// ------------------------------------------------------------ SELL-32 SpMV + epilogue
+// For layouts whose rows are short and of similar length (A^T of every config):
+// warp = slice of 32 consecutive rows, lane = row.  Column indices and values are
+// streamed straight from HBM (coalesced: 128 B / 256 B per warp per k, evict-first),
+// the gathered vector goes through L1 (no shared memory is used, so L1 keeps its
+// full capacity for the reused entries), and the fused epilogue gets the row sum
+// in the lane that owns the row.  Sum order = CSR order (k ascending).
+struct DevSell {
+    const int64_t* __restrict__ sp;
+    const int32_t* __restrict__ col;
+    const double* __restrict__ val;
+    int32_t rows, nslice;
+};
+
+constexpr int TPB_SELL = 256;
+constexpr int SELL_U = 8;   // entries per lane in flight
+
+template <int NV, class Epi>
+__global__ void __launch_bounds__(TPB_SELL)
+k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr,
+       double* red)
+{
+    constexpr int NS = Epi::NS;
+    constexpr int NVEC = Epi::NVEC;
+    __shared__ int s_go;
+    if (threadIdx.x == 0) {
+        s_go = gate_open(gate, ctl);
+        if (s_go && gate.active && blockIdx.x == 0) gate.active[gate.node] = 1;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    Epi e = epi;
+    e.load(ctl);
+    const double* vin[NVEC > 0 ? NVEC : 1];
+#pragma unroll
+    for (int v = 0; v < NVEC; ++v) vin[v] = e.vec(v);
+    const double* __restrict__ v0 = vs0.get(ctl);
+    const double* __restrict__ v1 = vs1.get(ctl);
+    double acc[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (TPB_SELL / 32);
+    for (int s = (blockIdx.x * TPB_SELL + threadIdx.x) >> 5; s < M.nslice; s += nw) {
+        const int64_t b = M.sp[s];
+        const int len = (int)((M.sp[s + 1] - b) >> 5);
+        const int r = s * 32 + lane;
+        // the epilogue's per-row inputs do not depend on the sum: start them now
+        if (r < M.rows)
+#pragma unroll
+            for (int v = 0; v < NVEC; ++v)
+                if (vin[v]) asm volatile("prefetch.global.L1 [%0];" ::"l"(vin[v] + r));
+        const int32_t* cp = M.col + b + lane;
+        const double* vp = M.val + b + lane;
+        double sm[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sm[v] = 0.0;
+        for (int k0 = 0; k0 < len; k0 += SELL_U) {
+            int c[SELL_U];
+            double a[SELL_U], g[SELL_U], g2[SELL_U];
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u) {
+                const bool ok = k0 + u < len;
+                c[u] = ok ? __ldcs(cp + (int64_t)(k0 + u) * 32) : -1;
+                a[u] = ok ? __ldcs(vp + (int64_t)(k0 + u) * 32) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u) {
+                g[u] = c[u] >= 0 ? __ldg(&v0[c[u]]) : 0.0;
+                if (NV > 1) g2[u] = c[u] >= 0 ? __ldg(&v1[c[u]]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u) {
+                if (c[u] >= 0) {
+                    sm[0] += a[u] * g[u];
+                    if (NV > 1) sm[NV - 1] += a[u] * g2[u];
+                }
+            }
+        }
+        if (r < M.rows) e.row(r, sm, vin, r, acc);
+    }
+    grid_finalize<NS, TPB_SELL>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+}
+
 // Elementwise pass over [0, N) with reductions and a device-side finalize.
 template <class Op>
 __global__ void __launch_bounds__(TPB)

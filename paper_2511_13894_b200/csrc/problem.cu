@@ -5,6 +5,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -128,6 +129,69 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     plan.long_ents.alloc(1);
     if (nl) CPD_CUDA(cudaMemcpy(plan.long_row.p, lrows.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice));
     CPD_CUDA(cudaMemcpy(plan.long_ptr.p, lptr.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice));
+}
+
+// ------------------------------------------------------------ SELL-32
+__global__ void k_sell_len(int32_t rows, int32_t nslice, const int32_t* p, int64_t* len)
+{
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslice;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        int32_t mx = 0;
+        const int64_t r1 = std::min<int64_t>((s + 1) * 32, rows);
+        for (int64_t r = s * 32; r < r1; ++r) mx = max(mx, p[r + 1] - p[r]);
+        len[s] = (int64_t)mx * 32;
+    }
+}
+
+// one thread per (slice, lane): row r's entries, then padding (-1, 0.0)
+__global__ void k_sell_fill(int32_t rows, int32_t nslice, const int32_t* p, const int32_t* j, const double* x,
+                            const int64_t* sp, int32_t* scol, double* sval)
+{
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)nslice * 32;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t >> 5, lane = t & 31, r = t;
+        const int64_t b = sp[s], len = (sp[s + 1] - b) >> 5;
+        const int64_t q0 = r < rows ? p[r] : 0, n = r < rows ? p[r + 1] - p[r] : 0;
+        for (int64_t k = 0; k < len; ++k) {
+            const int64_t d = b + k * 32 + lane;
+            scol[d] = k < n ? j[q0 + k] : -1;
+            sval[d] = k < n ? x[q0 + k] : 0.0;
+        }
+    }
+}
+
+void build_sell(Matrix& M, int64_t nnz, double max_ratio)
+{
+    Sell& S = M.sell;
+    S.on = false;
+    const int32_t rows = M.rows;
+    const int32_t ns = (int32_t)(((int64_t)rows + 31) / 32);
+    if (nnz == 0 || rows == 0) return;
+    DBuf<int64_t> len((size_t)ns + 1);
+    CPD_CUDA(cudaMemset(len.p, 0, sizeof(int64_t) * ((size_t)ns + 1)));
+    const int g = (int)std::min<int64_t>(((int64_t)ns + 255) / 256, 4096);
+    k_sell_len<<<g, 256>>>(rows, ns, M.p.p, len.p);
+    CPD_CUDA(cudaGetLastError());
+    S.sp.alloc((size_t)ns + 1);
+    size_t tb = 0;
+    CPD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, len.p, S.sp.p, ns + 1));
+    DBuf<unsigned char> tmp(tb);
+    CPD_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, len.p, S.sp.p, ns + 1));
+    int64_t padded = 0;
+    CPD_CUDA(cudaMemcpy(&padded, S.sp.p + ns, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    S.padded = padded;
+    if ((double)padded > max_ratio * (double)nnz) {
+        S.sp.free();
+        return;
+    }
+    S.col.alloc((size_t)padded);
+    S.val.alloc((size_t)padded);
+    const int g2 = (int)std::min<int64_t>(((int64_t)ns * 32 + 255) / 256, 65536);
+    k_sell_fill<<<g2, 256>>>(rows, ns, M.p.p, M.j.p, M.x.p, S.sp.p, S.col.p, S.val.p);
+    CPD_CUDA(cudaGetLastError());
+    CPD_CUDA(cudaDeviceSynchronize());
+    S.nslice = ns;
+    S.on = true;
 }
 
 // ------------------------------------------------------------ validation
@@ -426,6 +490,12 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         CPD_CUDA(cudaMemcpy(htp.data(), P->AT.p.p, sizeof(int32_t) * htp.size(), cudaMemcpyDeviceToHost));
         build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.plan);
         build_plan(n, m, htp, P->AT.p.p, P->AT.j.p, P->AT.plan);
+        // SELL-32 where the rows are short and even (padding <= 25%); CPD_SELL=0 disables
+        const char* se = getenv("CPD_SELL");
+        const bool sell_ok = !(se && se[0] == '0');
+        // (A^T only: for A the dual epilogue's four staged vectors favour the TMA plan
+        // kernel, measured on C4 — profiles/r01_kernel_iterations.md)
+        if (sell_ok && nnz <= (int64_t)n * 64) build_sell(P->AT, nnz, 1.25);
         CPD_CUDA(cudaDeviceSynchronize());
     } catch (...) {
         delete P;

@@ -117,6 +117,23 @@ template <int NV, class Epi>
 void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel v1, const Epi& epi,
                  Gate g, double* red)
 {
+    if (M.sell.on) {
+        static int sgrid = 0, ssms = 0;
+        {
+            std::lock_guard<std::mutex> lk(g_grid_mu);
+            if (!sgrid || ssms != cx.P->num_sms) {
+                int nb = 0;
+                CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sell<NV, Epi>, TPB_SELL, 0));
+                ssms = cx.P->num_sms;
+                sgrid = std::max(1, nb) * ssms;
+            }
+        }
+        const int gr = std::max(1, std::min<int>(sgrid, (M.sell.nslice + 7) / 8));
+        k_sell<NV, Epi><<<gr, TPB_SELL, 0, cx.st>>>(M.dsell(), v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p, red);
+        CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
+        return;
+    }
     constexpr size_t SMEM = sizeof(SpmvSmem<NV, Epi::NVEC>);
     static int grid = 0, sms = 0;
     {

@@ -21,11 +21,16 @@ def main():
     ap.add_argument("--libs", default=_build.LIB)
     ap.add_argument("--iters", type=int, default=256)
     ap.add_argument("--corner", type=int, default=0)
+    ap.add_argument("--env", default="", help="';'-separated variants of K=V,K=V env settings per run")
     a = ap.parse_args()
     t = time.time()
     lp = lpgen.config(a.config)
     print(f"gen {time.time() - t:.1f}s", flush=True)
-    for path in a.libs.split(","):
+    runs = [(p, e) for p in a.libs.split(",") for e in (a.env.split(";") if a.env else [""])]
+    for path, env in runs:
+        for kv in filter(None, env.split(",")):
+            k, v = kv.split("=")
+            os.environ[k] = v
         _build.LIB = path
         cpd._lib = None
         P = cpd.Problem.from_lp(lp)
@@ -36,7 +41,7 @@ def main():
         S.step(a.iters)
         wall = time.time() - t0
         kt = S.kernel_times()
-        line = [f"{os.path.basename(path)}: {a.iters / wall:.1f} it/s wall"]
+        line = [f"{os.path.basename(path)} [{env}]: {a.iters / wall:.1f} it/s wall"]
         for k, (ms, n) in kt.items():
             if n:
                 b = S.kernel_bytes(k)
