@@ -65,13 +65,15 @@ struct Plan {
     DBuf<PlanEntry> ent;
     DBuf<int32_t> long_row, long_ptr, long_ents;
     int32_t nent = 0, nlong = 0;
+    int32_t warp = 0;     // 1: warp-item plan for k_csrw (<= 32 rows / <= WCAP nnz per item)
+    std::vector<int32_t> seg;   // item ranges launched separately: rows items, then one per column slab
     int64_t rows_entries = 0, single_entries = 0, long_pieces = 0;
     int32_t nslab = 1;
 };
 // rows x cols CSR with device column array d_col; long rows are cut into CAP pieces
 // at column-slab boundaries and their pieces ordered slab-major.
 void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rowptr, const int32_t* d_p,
-                const int32_t* d_col, Plan& plan);
+                const int32_t* d_col, Plan& plan, bool warp = false);
 
 // SELL-32 copy of a CSR layout whose rows are short and of similar length
 // (DESIGN.md §6): slices of 32 consecutive rows, each padded to its longest row,

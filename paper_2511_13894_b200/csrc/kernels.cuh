@@ -33,6 +33,9 @@ constexpr int SINGLE_MIN = 256;  // a row with more nonzeros gets an entry of it
 constexpr int NSTAGE = 3;      // TMA pipeline depth (stages per CTA)
 constexpr int NVECMAX = 5;     // staged per-row vectors per entry
 constexpr int NSMAX = 12;      // max scalars an epilogue reduces
+constexpr int WCAP_ROWS = 1024;  // k_csrw: nonzeros per rows item (<= 32 rows)
+constexpr int WLONG = 512;       // k_csrw: a longer row is cut into pieces
+constexpr int WCAP_LONG = 2048;  // k_csrw: nonzeros per long-row piece
 
 enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2 };
 enum { ST_RUNNING = -1, ST_CONVERGED = 0, ST_ITER_LIMIT = 1, ST_TIME_LIMIT = 2, ST_FAIL = 3 };
@@ -49,6 +52,7 @@ struct DevPlan {
     const PlanEntry* ent;
     int32_t nent;
     int32_t nlong;
+    int32_t pslot;             // warp partials per piece slot (GW: k_spmv, 1: k_csrw)
     const int32_t* long_row;   // [nlong] row index of each long row
     const int32_t* long_ptr;   // [nlong + 1] piece slots of each long row (column order)
     const int32_t* long_ents;  // unused (kept for layout stability)
@@ -255,13 +259,13 @@ __device__ __forceinline__ void grid_finalize(double (&acc)[NS], double* bpart, 
 
 // Block partial only (no combine): the finishing kernel combines it.
 template <int NS, int NT = TPB>
-__device__ __forceinline__ void block_partial(double (&acc)[NS], double* bpart)
+__device__ __forceinline__ void block_partial(double (&acc)[NS], double* bpart, int prev = 0)
 {
     __shared__ double sw[NT / 32][NS];
     block_sum<NS, NT>(acc, sw);
     if (threadIdx.x == 0)
 #pragma unroll
-        for (int s = 0; s < NS; ++s) bpart[(size_t)blockIdx.x * NS + s] = acc[s];
+        for (int s = 0; s < NS; ++s) bpart[(size_t)(prev + blockIdx.x) * NS + s] = acc[s];
 }
 
 // ------------------------------------------------------------ TMA / mbarrier (sm_90+ PTX, used on sm_100a)
@@ -691,7 +695,7 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
         double sm[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) sm[v] = 0.0;
-        const int64_t t0 = (int64_t)P.long_ptr[l] * GW, t1 = (int64_t)P.long_ptr[l + 1] * GW;
+        const int64_t t0 = (int64_t)P.long_ptr[l] * P.pslot, t1 = (int64_t)P.long_ptr[l + 1] * P.pslot;
         for (int64_t t = t0 + threadIdx.x; t < t1; t += TPB)
 #pragma unroll
             for (int v = 0; v < NV; ++v) sm[v] += __ldcg(&P.lpart[t * 2 + v]);
@@ -719,7 +723,10 @@ struct DevSell {
 };
 
 constexpr int TPB_SELL = 256;
-constexpr int SELL_U = 8;   // entries per lane in flight
+#ifndef CPD_SELL_U
+#define CPD_SELL_U 8
+#endif
+constexpr int SELL_U = CPD_SELL_U;   // entries per lane in flight
 
 template <int NV, class Epi>
 __global__ void __launch_bounds__(TPB_SELL)
@@ -747,45 +754,230 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
     for (int s = 0; s < NS; ++s) acc[s] = 0.0;
     const int lane = threadIdx.x & 31;
     const int nw = gridDim.x * (TPB_SELL / 32);
+    __shared__ double vst[TPB_SELL / 32][(NVEC > 0 ? NVEC : 1) * 32];
     for (int s = (blockIdx.x * TPB_SELL + threadIdx.x) >> 5; s < M.nslice; s += nw) {
         const int64_t b = M.sp[s];
         const int len = (int)((M.sp[s + 1] - b) >> 5);
         const int r = s * 32 + lane;
-        // the epilogue's per-row inputs do not depend on the sum: start them now
+        // the epilogue's per-row inputs do not depend on the sum: load them now
+        // (streamed, evict-first) into this warp's stage
+        double* stg = vst[threadIdx.x >> 5];
         if (r < M.rows)
 #pragma unroll
-            for (int v = 0; v < NVEC; ++v)
-                if (vin[v]) asm volatile("prefetch.global.L1 [%0];" ::"l"(vin[v] + r));
+            for (int v = 0; v < NVEC; ++v) stg[v * 32 + lane] = vin[v] ? __ldcs(vin[v] + r) : 0.0;
         const int32_t* cp = M.col + b + lane;
         const double* vp = M.val + b + lane;
         double sm[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) sm[v] = 0.0;
-        for (int k0 = 0; k0 < len; k0 += SELL_U) {
-            int c[SELL_U];
-            double a[SELL_U], g[SELL_U], g2[SELL_U];
+        // two-stage software pipeline over rounds of SELL_U entries per lane
+        auto ldround = [&](int (&cc)[SELL_U], double (&aa)[SELL_U], int k0) {
 #pragma unroll
             for (int u = 0; u < SELL_U; ++u) {
                 const bool ok = k0 + u < len;
-                c[u] = ok ? __ldcs(cp + (int64_t)(k0 + u) * 32) : -1;
-                a[u] = ok ? __ldcs(vp + (int64_t)(k0 + u) * 32) : 0.0;
+                cc[u] = ok ? __ldcs(cp + (int64_t)(k0 + u) * 32) : -1;
+                aa[u] = ok ? __ldcs(vp + (int64_t)(k0 + u) * 32) : 0.0;
             }
+        };
+        int c[SELL_U];
+        double a[SELL_U];
+        ldround(c, a, 0);
+        for (int k0 = 0; k0 < len; k0 += SELL_U) {
+            double g[SELL_U], g2[SELL_U];
 #pragma unroll
             for (int u = 0; u < SELL_U; ++u) {
                 g[u] = c[u] >= 0 ? __ldg(&v0[c[u]]) : 0.0;
                 if (NV > 1) g2[u] = c[u] >= 0 ? __ldg(&v1[c[u]]) : 0.0;
             }
+            int cn[SELL_U];
+            double an[SELL_U];
+            ldround(cn, an, k0 + SELL_U);
 #pragma unroll
             for (int u = 0; u < SELL_U; ++u) {
                 if (c[u] >= 0) {
                     sm[0] += a[u] * g[u];
                     if (NV > 1) sm[NV - 1] += a[u] * g2[u];
                 }
+                c[u] = cn[u];
+                a[u] = an[u];
             }
         }
-        if (r < M.rows) e.row(r, sm, vin, r, acc);
+        if (r < M.rows) {
+            const double* vs[NVEC > 0 ? NVEC : 1];
+#pragma unroll
+            for (int v = 0; v < NVEC; ++v) vs[v] = stg + v * 32;
+            e.row(r, sm, vs, lane, acc);
+        }
     }
     grid_finalize<NS, TPB_SELL>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+}
+
+// ------------------------------------------------------------ warp-item CSR SpMV + epilogue
+// For general CSR layouts (A): one warp per plan item, no shared memory.
+//  rows item (<= 32 rows, <= WCAP_ROWS nonzeros): the item's nonzeros are streamed
+//    coalesced (lane-strided, WU per lane in flight), each lane finds the row of its
+//    element by a 5-step shuffle search over the row starts, a segmented warp scan
+//    sums each row's run inside the 32-element round, and the lane that owns the
+//    row (lane = row) adds the run's total; then lane = row runs the epilogue.
+//  long-row piece (<= WCAP_LONG nonzeros inside one column slab): lane-strided sum,
+//    warp xor-reduction, one partial per piece for k_finish.
+// Fixed order for a fixed plan: deterministic.
+constexpr int TPB_W = 256;
+constexpr int WU = 4;
+
+template <int NV, class Epi>
+__global__ void __launch_bounds__(TPB_W)
+k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr,
+       double* red, int prev, int fin)
+{
+    constexpr int NS = Epi::NS;
+    constexpr int NVEC = Epi::NVEC;
+    __shared__ int s_go;
+    if (threadIdx.x == 0) {
+        s_go = gate_open(gate, ctl);
+        if (s_go && gate.active && blockIdx.x == 0) gate.active[gate.node] = 1;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    Epi e = epi;
+    e.load(ctl);
+    const double* vin[NVEC > 0 ? NVEC : 1];
+#pragma unroll
+    for (int v = 0; v < NVEC; ++v) vin[v] = e.vec(v);
+    const double* __restrict__ v0 = vs0.get(ctl);
+    const double* __restrict__ v1 = vs1.get(ctl);
+    double acc[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (TPB_W / 32);
+    __shared__ double vst[TPB_W / 32][(NVEC > 0 ? NVEC : 1) * 32];
+    for (int it = (blockIdx.x * TPB_W + threadIdx.x) >> 5; it < P.nent; it += nw) {
+        const PlanEntry E = P.ent[it];
+        const int p0 = E.p0, T = E.p1 - E.p0;
+        // one round: WU lane-strided entries from `base` (streamed, evict-first)
+        auto ldround = [&](int (&cc)[WU], double (&aa)[WU], int base) {
+#pragma unroll
+            for (int u = 0; u < WU; ++u) {
+                const int q = base + 32 * u + lane;
+                cc[u] = q < T ? __ldcs(M.j + p0 + q) : -1;
+                aa[u] = q < T ? __ldcs(M.x + p0 + q) : 0.0;
+            }
+        };
+        if (E.b >= 0) {
+            const int r0 = E.a, nr = E.b - E.a;
+            const int rs = lane < nr ? M.p[r0 + lane] - p0 : 0x7fffffff;   // start of row `lane`
+            const int re = lane < nr ? M.p[r0 + lane + 1] - p0 : 0;         // its end
+            double* stg = vst[threadIdx.x >> 5];
+            if (lane < nr)
+#pragma unroll
+                for (int v = 0; v < NVEC; ++v) stg[v * 32 + lane] = vin[v] ? __ldcs(vin[v] + r0 + lane) : 0.0;
+            double racc[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) racc[v] = 0.0;
+            // two-stage software pipeline: the next round's indices / values are in
+            // flight while this round's gathers are
+            int c[WU];
+            double a[WU];
+            ldround(c, a, 0);
+            for (int base = 0; base < T; base += 32 * WU) {
+                double g[WU][NV];
+#pragma unroll
+                for (int u = 0; u < WU; ++u) {
+                    g[u][0] = c[u] >= 0 ? __ldg(&v0[c[u]]) : 0.0;
+                    if (NV > 1) g[u][NV - 1] = c[u] >= 0 ? __ldg(&v1[c[u]]) : 0.0;
+                }
+                int cn[WU];
+                double an[WU];
+                ldround(cn, an, base + 32 * WU);
+#pragma unroll
+                for (int u = 0; u < WU; ++u) {
+                    const int rb = base + 32 * u;
+                    if (rb >= T) break;   // warp-uniform
+                    const int q = rb + lane;
+                    // row of element q: largest i < nr with rs_i <= q (invalid q: own key)
+                    int lo = 0;
+#pragma unroll
+                    for (int st = 16; st > 0; st >>= 1) {
+                        const int cand = lo + st;
+                        const int rv = __shfl_sync(FULL, rs, cand & 31);
+                        if (cand < nr && rv <= q) lo = cand;
+                    }
+                    const int key = q < T ? lo : 64 + lane;
+                    double sv[NV];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) sv[v] = a[u] * g[u][v];
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int kt = __shfl_up_sync(FULL, key, d);
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) {
+                            const double t = __shfl_up_sync(FULL, sv[v], d);
+                            if (lane >= d && kt == key) sv[v] += t;
+                        }
+                    }
+                    // owner lane = row: its run in this round ends at min(re, rb + 32) - 1
+                    const bool hit = lane < nr && rs < rb + 32 && re > rb && re > rs;
+                    const int pos = hit ? min(re, rb + 32) - 1 - rb : 0;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        const double t = __shfl_sync(FULL, sv[v], pos);
+                        if (hit) racc[v] += t;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < WU; ++u) {
+                    c[u] = cn[u];
+                    a[u] = an[u];
+                }
+            }
+            if (lane < nr) {
+                const double* vs[NVEC > 0 ? NVEC : 1];
+#pragma unroll
+                for (int v = 0; v < NVEC; ++v) vs[v] = stg + v * 32;
+                e.row(r0 + lane, racc, vs, lane, acc);
+            }
+        } else {
+            double sm[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) sm[v] = 0.0;
+            int c[WU];
+            double a[WU];
+            ldround(c, a, 0);
+            for (int base = 0; base < T; base += 32 * WU) {
+                double g[WU][NV];
+#pragma unroll
+                for (int u = 0; u < WU; ++u) {
+                    g[u][0] = c[u] >= 0 ? __ldg(&v0[c[u]]) : 0.0;
+                    if (NV > 1) g[u][NV - 1] = c[u] >= 0 ? __ldg(&v1[c[u]]) : 0.0;
+                }
+                int cn[WU];
+                double an[WU];
+                ldround(cn, an, base + 32 * WU);
+#pragma unroll
+                for (int u = 0; u < WU; ++u) {
+                    if (c[u] >= 0) {
+                        sm[0] += a[u] * g[u][0];
+                        if (NV > 1) sm[NV - 1] += a[u] * g[u][NV - 1];
+                    }
+                    c[u] = cn[u];
+                    a[u] = an[u];
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sm[v] += __shfl_xor_sync(FULL, sm[v], o);
+            if (lane == 0)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) P.lpart[(size_t)E.a * 2 + v] = sm[v];
+        }
+    }
+    if (fin)
+        grid_finalize<NS, TPB_W>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+    else
+        block_partial<NS, TPB_W>(acc, bpart, prev);
 }
 
 // Elementwise pass over [0, N) with reductions and a device-side finalize.
@@ -938,7 +1130,8 @@ struct EpiPrimalT {
         const double xp = proj(x - tau * z, lo, hi);
         xn[j] = xp;
         const double xa = vin[2][li];
-        xan[j] = xa + (xp - xa) * inv_t;   // (x+ - x_avg)/t as a multiply (<= 1 ulp)
+        // averages are read once per iteration: streamed (evict-first) so L2 keeps x+
+        __stcs(&xan[j], xa + (xp - xa) * inv_t);   // (x+ - x_avg)/t as a multiply (<= 1 ulp)
         acc[0] += cj * x;
         dual_terms(z, lo, hi, acc[1], acc[2]);
         acc[3] += isfinite(xp) ? 0.0 : 1.0;
@@ -993,7 +1186,7 @@ struct EpiDual {
         y[i] = yp;
         ax[i] = axn;
         const double yav = vin[3][li];
-        ya[i] = yav + (yp - yav) * inv_t;
+        __stcs(&ya[i], yav + (yp - yav) * inv_t);
         const double r = bi - axn;
         acc[0] += r * r;
         acc[1] += bi * yp;

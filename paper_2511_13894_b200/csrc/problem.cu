@@ -44,8 +44,13 @@ __global__ void k_slab_pos(int32_t nl, int32_t nb, const int32_t* lrows, const i
 // (while the CTAs sweep one slab, that slab of the gathered vector stays in L2);
 // k_finish sums its pieces and applies its epilogue.
 void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, const int32_t* d_p,
-                const int32_t* d_col, Plan& plan)
+                const int32_t* d_col, Plan& plan, bool warp)
 {
+    // TMA plan: <= RMAX rows / CAP nnz per entry, rows > SINGLE_MIN long, CAP pieces.
+    // warp plan (k_csrw): <= 32 rows / WCAP_ROWS nnz per item, rows > WLONG long, WCAP_LONG pieces.
+    const int64_t cap_rows = warp ? WCAP_ROWS : CAP, max_rows = warp ? 32 : RMAX;
+    const int64_t long_min = warp ? WLONG : SINGLE_MIN, piece = warp ? WCAP_LONG : CAP;
+    plan.warp = warp ? 1 : 0;
     std::vector<PlanEntry> ent;
     std::vector<int32_t> lrows;
     int64_t nrows_e = 0, nsingle = 0;
@@ -59,7 +64,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     };
     for (int32_t r = 0; r < rows; ++r) {
         const int64_t len = (int64_t)rp[r + 1] - rp[r];
-        if (len > SINGLE_MIN) {
+        if (len > long_min) {
             // long row: pieces (any length > SINGLE_MIN; k_finish applies its epilogue)
             flush(r);
             lrows.push_back(r);
@@ -67,7 +72,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
             cur = 0;
             continue;
         }
-        if (cur + len > CAP || (r - r0) >= RMAX) {
+        if (cur + len > cap_rows || (r - r0) >= max_rows) {
             flush(r);
             r0 = r;
             cur = 0;
@@ -96,8 +101,8 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
         int32_t a = rp[r];
         for (int32_t s = 0; s < nslab; ++s) {
             const int32_t b = (s + 1 < nslab) ? pos[(size_t)l * nb + s] : rp[r + 1];
-            for (int32_t q = a; q < b; q += CAP)
-                by_slab[s].push_back(PlanEntry{r, -1 - l, q, std::min(q + CAP, b)});
+            for (int32_t q = a; q < b; q += (int32_t)piece)
+                by_slab[s].push_back(PlanEntry{r, -1 - l, q, (int32_t)std::min<int64_t>((int64_t)q + piece, b)});
             a = b;
         }
     }
@@ -108,12 +113,16 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     for (int32_t l = 0; l < nl; ++l) lptr[l + 1] += lptr[l];
     std::vector<int32_t> next(lptr.begin(), lptr.end() - 1), lents;
     int64_t npieces = 0;
-    for (int32_t s = 0; s < nslab; ++s)
+    plan.seg.assign(1, 0);
+    plan.seg.push_back((int32_t)ent.size());
+    for (int32_t s = 0; s < nslab; ++s) {
+        if (!by_slab[s].empty()) plan.seg.push_back((int32_t)(ent.size() + by_slab[s].size()));
         for (PlanEntry E : by_slab[s]) {
             E.a = next[-1 - E.b]++;   // slab-major visit == column order within each row
             ent.push_back(E);
             ++npieces;
         }
+    }
     if (ent.size() > (size_t)INT32_MAX / 2) throw Error(CPD_E_DIM, "plan too large");
     plan.nent = (int32_t)ent.size();
     plan.nlong = nl;
@@ -488,7 +497,10 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         std::vector<int32_t> hp((size_t)m + 1), htp((size_t)n + 1);
         CPD_CUDA(cudaMemcpy(hp.data(), P->A.p.p, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
         CPD_CUDA(cudaMemcpy(htp.data(), P->AT.p.p, sizeof(int32_t) * htp.size(), cudaMemcpyDeviceToHost));
-        build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.plan);
+        // A: warp-item plan for k_csrw unless CPD_WARP=0 (then the TMA plan of k_spmv)
+        const char* we = getenv("CPD_WARP");
+        const bool warpA = !(we && we[0] == '0');
+        build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.plan, warpA);
         build_plan(n, m, htp, P->AT.p.p, P->AT.j.p, P->AT.plan);
         // SELL-32 where the rows are short and even (padding <= 25%); CPD_SELL=0 disables
         const char* se = getenv("CPD_SELL");

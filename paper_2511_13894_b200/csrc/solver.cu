@@ -42,7 +42,9 @@ Ctx::Ctx(const cpd_problem* p) : P(p)
     std::memset(h_aux, 0, sizeof(Ctl));
     ctl = ctl_main.p;
     h_ctl = h_main;
-    bpart.alloc((size_t)p->num_sms * 16 * NSMAX);
+    // block partials: every segment launch of a warp plan (<= 8 blocks/SM each) + k_finish
+    const size_t nseg = std::max(p->A.plan.seg.size(), p->AT.plan.seg.size());
+    bpart.alloc((size_t)p->num_sms * (8 * (nseg + 1) + 16) * NSMAX);
     ctr.alloc(1);
     CPD_CUDA(cudaMemset(ctr.p, 0, sizeof(unsigned)));
     const Plan& pa = p->A.plan;
@@ -70,13 +72,15 @@ Ctx::~Ctx()
 DevPlan Ctx::planA() const
 {
     const Plan& pl = P->A.plan;
-    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p, lpartA.p};
+    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p,
+                   lpartA.p};
 }
 
 DevPlan Ctx::planAT() const
 {
     const Plan& pl = P->AT.plan;
-    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p, lpartAT.p};
+    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p,
+                   lpartAT.p};
 }
 
 void Ctx::pull_ctl()
@@ -132,6 +136,48 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         k_sell<NV, Epi><<<gr, TPB_SELL, 0, cx.st>>>(M.dsell(), v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p, red);
         CPD_CUDA(cudaGetLastError());
         ++cx.launches;
+        return;
+    }
+    if (dp.pslot == 1) {   // warp-item plan
+        static int wgrid = 0, wsms = 0;
+        {
+            std::lock_guard<std::mutex> lk(g_grid_mu);
+            if (!wgrid || wsms != cx.P->num_sms) {
+                int nb = 0;
+                CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_csrw<NV, Epi>, TPB_W, 0));
+                wsms = cx.P->num_sms;
+                wgrid = std::max(1, nb) * wsms;
+            }
+        }
+        // one launch per item segment (rows items, then each column slab's pieces), so
+        // all warps sweep one slab of the gathered vector at a time (L2-resident)
+        const std::vector<int32_t>& seg = M.plan.seg;
+        const bool single = dp.nlong == 0;
+        int prev = 0;
+        Gate gs = g;
+        for (size_t k = 0; k + 1 < seg.size() || (k == 0 && seg.size() < 2); ++k) {
+            DevPlan ds = dp;
+            const int a = seg.size() >= 2 ? seg[k] : 0, b = seg.size() >= 2 ? seg[k + 1] : dp.nent;
+            if (b <= a && !single) continue;
+            ds.ent = dp.ent + a;
+            ds.nent = b - a;
+            const int gr = std::max(1, std::min<int>(wgrid, (ds.nent + 7) / 8));
+            k_csrw<NV, Epi><<<gr, TPB_W, 0, cx.st>>>(M.dev(), ds, v0, v1, epi, gs, cx.ctl, cx.bpart.p, cx.ctr.p,
+                                                     red, prev, single ? 1 : 0);
+            CPD_CUDA(cudaGetLastError());
+            ++cx.launches;
+            gs.active = nullptr;
+            prev += gr;
+            if (single) break;
+        }
+        if (dp.nlong > 0) {
+            const int gf = std::max(1, std::min(cx.P->num_sms * 8, dp.nlong));
+            Gate g2 = g;
+            g2.active = nullptr;
+            k_finish<NV, Epi><<<gf, TPB, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, prev, red);
+            CPD_CUDA(cudaGetLastError());
+            ++cx.launches;
+        }
         return;
     }
     constexpr size_t SMEM = sizeof(SpmvSmem<NV, Epi::NVEC>);

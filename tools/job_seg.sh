@@ -1,0 +1,8 @@
+set -x
+OUT=gpurun_out/r1s2e; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || exit 1
+for U in 4 12; do CPD_LIB=/tmp/libcpd_u$U.so CPD_BUILD_TAG=_u$U CPD_NVCC_DEFS="-DCPD_SELL_U=$U" python -c "from paper_2511_13894_b200 import _build; _build.build(force=True)" > $OUT/build_u$U.log 2>&1; done
+timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; tail -5 $OUT/pytest_gpu.log
+timeout 600 python tools/kern_time.py --config c5 --corner 1 --libs paper_2511_13894_b200/libcpd.so,/tmp/libcpd_u4.so,/tmp/libcpd_u12.so 2>&1 | tee $OUT/kt_c5.txt
+timeout 600 python tools/kern_time.py --config c5 --env "CPD_WARP=0" 2>&1 | tee -a $OUT/kt_c5.txt
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct --kernel-name-base demangled -k "regex:k_csrw|k_finish|k_sell" -s 10 -c 12 python tools/prof_run.py --iters 3 > $OUT/ncu_seg.log 2>&1; tail -60 $OUT/ncu_seg.log
