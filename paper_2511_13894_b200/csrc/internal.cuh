@@ -67,6 +67,9 @@ struct Plan {
     int32_t nent = 0, nlong = 0;
     int32_t warp = 0;     // 1: warp-item plan for k_csrw (<= 32 rows / <= WCAP nnz per item)
     std::vector<int32_t> seg;   // item ranges launched separately: rows items, then one per column slab
+    int32_t nheavy = 0, nhb = 0;          // heavy rows (k_dense) and column blocks of HB
+    DBuf<PlanEntry> dense_ent;            // {slot, block, q0, q1} grouped by block
+    DBuf<int32_t> dense_ptr;              // [nhb + 1] item range of each block
     int64_t rows_entries = 0, single_entries = 0, long_pieces = 0;
     int32_t nslab = 1;
 };

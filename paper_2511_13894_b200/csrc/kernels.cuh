@@ -35,7 +35,14 @@ constexpr int NVECMAX = 5;     // staged per-row vectors per entry
 constexpr int NSMAX = 12;      // max scalars an epilogue reduces
 constexpr int WCAP_ROWS = 1024;  // k_csrw: nonzeros per rows item (<= 32 rows)
 constexpr int WLONG = 512;       // k_csrw: a longer row is cut into pieces
-constexpr int WCAP_LONG = 2048;  // k_csrw: nonzeros per long-row piece
+#ifndef CPD_WCAP_LONG
+#define CPD_WCAP_LONG 2048
+#endif
+constexpr int WCAP_LONG = CPD_WCAP_LONG;  // k_csrw: nonzeros per long-row piece
+constexpr int HEAVY_MIN = 65536; // k_dense: rows with at least this many nonzeros
+constexpr int HB = 8192;         // k_dense: columns per dense block (64 KB of the vector in smem)
+constexpr int DCHUNK = 512;      // k_dense: entries per item (balances the Zipf head across warps)
+constexpr int TPB_D = 512;
 
 enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2 };
 enum { ST_RUNNING = -1, ST_CONVERGED = 0, ST_ITER_LIMIT = 1, ST_TIME_LIMIT = 2, ST_FAIL = 3 };
@@ -53,6 +60,9 @@ struct DevPlan {
     int32_t nent;
     int32_t nlong;
     int32_t pslot;             // warp partials per piece slot (GW: k_spmv, 1: k_csrw)
+    int32_t nheavy, nhb;       // heavy rows / dense column blocks (k_dense)
+    const PlanEntry* dense_ent;   // {slot, block, q0, q1}: <= DCHUNK entries of one heavy row in one block
+    const int32_t* dense_ptr;     // [nhb + 1] items of each block
     const int32_t* long_row;   // [nlong] row index of each long row
     const int32_t* long_ptr;   // [nlong + 1] piece slots of each long row (column order)
     const int32_t* long_ents;  // unused (kept for layout stability)
@@ -723,13 +733,19 @@ struct DevSell {
 };
 
 constexpr int TPB_SELL = 256;
+#ifndef CPD_PRE
+#define CPD_PRE 0   // 1: epilogue inputs held in registers across the sum (more registers)
+#endif
 #ifndef CPD_SELL_U
 #define CPD_SELL_U 8
 #endif
 constexpr int SELL_U = CPD_SELL_U;   // entries per lane in flight
 
+#ifndef CPD_SELL_MINB
+#define CPD_SELL_MINB 4
+#endif
 template <int NV, class Epi>
-__global__ void __launch_bounds__(TPB_SELL)
+__global__ void __launch_bounds__(TPB_SELL, CPD_SELL_MINB)
 k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr,
        double* red)
 {
@@ -762,9 +778,15 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
         // the epilogue's per-row inputs do not depend on the sum: load them now
         // (streamed, evict-first) into this warp's stage
         double* stg = vst[threadIdx.x >> 5];
+#if CPD_PRE
+        double pre[NVEC > 0 ? NVEC : 1];   // in registers until the sum is done (no wait here)
+#pragma unroll
+        for (int v = 0; v < NVEC; ++v) pre[v] = (r < M.rows && vin[v]) ? __ldcs(vin[v] + r) : 0.0;
+#else
         if (r < M.rows)
 #pragma unroll
             for (int v = 0; v < NVEC; ++v) stg[v * 32 + lane] = vin[v] ? __ldcs(vin[v] + r) : 0.0;
+#endif
         const int32_t* cp = M.col + b + lane;
         const double* vp = M.val + b + lane;
         double sm[NV];
@@ -805,7 +827,12 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
         if (r < M.rows) {
             const double* vs[NVEC > 0 ? NVEC : 1];
 #pragma unroll
-            for (int v = 0; v < NVEC; ++v) vs[v] = stg + v * 32;
+            for (int v = 0; v < NVEC; ++v) {
+#if CPD_PRE
+                stg[v * 32 + lane] = pre[v];
+#endif
+                vs[v] = stg + v * 32;
+            }
             e.row(r, sm, vs, lane, acc);
         }
     }
@@ -825,8 +852,11 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
 constexpr int TPB_W = 256;
 constexpr int WU = 4;
 
+#ifndef CPD_W_MINB
+#define CPD_W_MINB 4
+#endif
 template <int NV, class Epi>
-__global__ void __launch_bounds__(TPB_W)
+__global__ void __launch_bounds__(TPB_W, CPD_W_MINB)
 k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr,
        double* red, int prev, int fin)
 {
@@ -870,9 +900,15 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
             const int rs = lane < nr ? M.p[r0 + lane] - p0 : 0x7fffffff;   // start of row `lane`
             const int re = lane < nr ? M.p[r0 + lane + 1] - p0 : 0;         // its end
             double* stg = vst[threadIdx.x >> 5];
+#if CPD_PRE
+            double pre[NVEC > 0 ? NVEC : 1];
+#pragma unroll
+            for (int v = 0; v < NVEC; ++v) pre[v] = (lane < nr && vin[v]) ? __ldcs(vin[v] + r0 + lane) : 0.0;
+#else
             if (lane < nr)
 #pragma unroll
                 for (int v = 0; v < NVEC; ++v) stg[v * 32 + lane] = vin[v] ? __ldcs(vin[v] + r0 + lane) : 0.0;
+#endif
             double racc[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) racc[v] = 0.0;
@@ -935,7 +971,12 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
             if (lane < nr) {
                 const double* vs[NVEC > 0 ? NVEC : 1];
 #pragma unroll
-                for (int v = 0; v < NVEC; ++v) vs[v] = stg + v * 32;
+                for (int v = 0; v < NVEC; ++v) {
+#if CPD_PRE
+                    stg[v * 32 + lane] = pre[v];
+#endif
+                    vs[v] = stg + v * 32;
+                }
                 e.row(r0 + lane, racc, vs, lane, acc);
             }
         } else {
@@ -978,6 +1019,70 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
         grid_finalize<NS, TPB_W>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
     else
         block_partial<NS, TPB_W>(acc, bpart, prev);
+}
+
+// ------------------------------------------------------------ heavy rows by dense column blocks
+// The few rows holding most nonzeros (C5: Zipf head) touch a large fraction of the
+// columns, so gathering their vector entries one 32-byte sector at a time costs
+// 4x the bytes in L2.  Instead each CTA takes a block of HB columns, loads that
+// block of the vector once (coalesced) into shared memory, and every warp sums the
+// block's entries of its heavy rows from shared memory; one partial per (row,
+// block) goes to the row's slot for k_finish (fixed order: deterministic).
+template <int NV>
+__global__ void __launch_bounds__(TPB_D)
+k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ctl* ctl)
+{
+    extern __shared__ __align__(16) double xs[];   // [NV][HB]
+    __shared__ int s_go;
+    if (threadIdx.x == 0) s_go = gate_open(gate, ctl);
+    __syncthreads();
+    if (!s_go) return;
+    const double* __restrict__ v0 = vs0.get(ctl);
+    const double* __restrict__ v1 = vs1.get(ctl);
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    constexpr int NWD = TPB_D / 32;
+    constexpr int DU = 8;
+    for (int blk = blockIdx.x; blk < P.nhb; blk += gridDim.x) {
+        const int j0 = blk * HB, nj = min(HB, cols - j0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nj; t += TPB_D) {
+            xs[t] = v0[j0 + t];
+            if (NV > 1) xs[HB + t] = v1[j0 + t];
+        }
+        __syncthreads();
+        const int i1 = P.dense_ptr[blk + 1];
+        for (int i = P.dense_ptr[blk] + w; i < i1; i += NWD) {
+            const PlanEntry E = P.dense_ent[i];
+            double sm[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) sm[v] = 0.0;
+            // <= DCHUNK entries: all of this lane's loads issued at once
+            for (int q = E.p0 + lane; q < E.p1; q += 32 * DU) {
+                int c[DU];
+                double a[DU];
+#pragma unroll
+                for (int u = 0; u < DU; ++u) {
+                    const int qq = q + 32 * u;
+                    c[u] = qq < E.p1 ? __ldcs(M.j + qq) - j0 : -1;
+                    a[u] = qq < E.p1 ? __ldcs(M.x + qq) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < DU; ++u)
+                    if (c[u] >= 0) {
+                        sm[0] += a[u] * xs[c[u]];
+                        if (NV > 1) sm[NV - 1] += a[u] * xs[HB + c[u]];
+                    }
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sm[v] += __shfl_xor_sync(FULL, sm[v], o);
+            if (lane == 0)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) P.lpart[(size_t)E.a * 2 + v] = sm[v];
+        }
+    }
 }
 
 // Elementwise pass over [0, N) with reductions and a device-side finalize.

@@ -22,12 +22,12 @@ constexpr int64_t SLAB_COLS = 4 << 20;
 
 // pos[l * nb + s - 1] = first position q of long row l with col[q] >= s * SLAB_COLS.
 __global__ void k_slab_pos(int32_t nl, int32_t nb, const int32_t* lrows, const int32_t* p,
-                           const int32_t* col, int32_t* pos)
+                           const int32_t* col, int32_t* pos, int64_t width = SLAB_COLS, int64_t first = 1)
 {
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (int64_t)nl * nb;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int32_t l = (int32_t)(idx / nb);
-        const int64_t target = (idx % nb + 1) * SLAB_COLS;
+        const int64_t target = (idx % nb + first) * width;
         const int32_t r = lrows[l];
         int32_t lo = p[r], hi = p[r + 1];
         while (lo < hi) {
@@ -93,10 +93,21 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
         CPD_CUDA(cudaGetLastError());
         CPD_CUDA(cudaMemcpy(pos.data(), dpos.p, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost));
     }
+    // heavy rows (warp plan): >= HEAVY_MIN nonzeros; their product runs by dense
+    // column blocks of HB columns (k_dense), one partial slot per block
+    const int32_t nhb = (int32_t)(((int64_t)cols + HB - 1) / HB);
+    std::vector<int32_t> heavy_l;
+    std::vector<char> is_heavy(nl, 0);
+    if (warp && cols >= 2 * HB)
+        for (int32_t l = 0; l < nl; ++l)
+            if ((int64_t)rp[lrows[l] + 1] - rp[lrows[l]] >= HEAVY_MIN) {
+                heavy_l.push_back(l);
+                is_heavy[l] = 1;
+            }
     // pieces[s] = list of (long id, q0, q1) in row order
     std::vector<std::vector<PlanEntry>> by_slab(nslab);
-    std::vector<std::vector<int32_t>> row_pieces_slab(nl);   // (slab, piece) order per row
     for (int32_t l = 0; l < nl; ++l) {
+        if (is_heavy[l]) continue;
         const int32_t r = lrows[l];
         int32_t a = rp[r];
         for (int32_t s = 0; s < nslab; ++s) {
@@ -110,7 +121,54 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     std::vector<int32_t> lptr(nl + 1, 0);
     for (int32_t s = 0; s < nslab; ++s)
         for (const PlanEntry& E : by_slab[s]) lptr[-1 - E.b + 1]++;
+    // heavy rows: block boundary positions (device binary search), then items of
+    // <= DCHUNK entries grouped by column block; a heavy row's slots are its items
+    // in column order
+    const int32_t nh = (int32_t)heavy_l.size();
+    std::vector<int32_t> hpos((size_t)nh * (nhb + 1));
+    if (nh > 0) {
+        std::vector<int32_t> hr(nh);
+        for (int32_t h = 0; h < nh; ++h) hr[h] = lrows[heavy_l[h]];
+        DBuf<int32_t> dhr(nh), dpos((size_t)nh * (nhb + 1));
+        CPD_CUDA(cudaMemcpy(dhr.p, hr.data(), sizeof(int32_t) * nh, cudaMemcpyHostToDevice));
+        const int64_t tot = (int64_t)nh * (nhb + 1);
+        k_slab_pos<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256>>>(nh, nhb + 1, dhr.p, d_p, d_col,
+                                                                            dpos.p, HB, 0);
+        CPD_CUDA(cudaGetLastError());
+        CPD_CUDA(cudaMemcpy(hpos.data(), dpos.p, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost));
+        for (int32_t h = 0; h < nh; ++h) {
+            int64_t cnt = 0;
+            for (int32_t b = 0; b < nhb; ++b) {
+                const int64_t len = (int64_t)hpos[(size_t)h * (nhb + 1) + b + 1] - hpos[(size_t)h * (nhb + 1) + b];
+                cnt += (len + DCHUNK - 1) / DCHUNK;
+            }
+            lptr[heavy_l[h] + 1] = (int32_t)cnt;
+        }
+    }
     for (int32_t l = 0; l < nl; ++l) lptr[l + 1] += lptr[l];
+    plan.nheavy = nh;
+    plan.nhb = nhb;
+    if (nh > 0) {
+        std::vector<std::vector<PlanEntry>> dl(nhb);
+        for (int32_t h = 0; h < nh; ++h) {
+            int32_t slot = lptr[heavy_l[h]];
+            for (int32_t b = 0; b < nhb; ++b) {
+                const int32_t q0 = hpos[(size_t)h * (nhb + 1) + b], q1 = hpos[(size_t)h * (nhb + 1) + b + 1];
+                for (int32_t q = q0; q < q1; q += DCHUNK)
+                    dl[b].push_back(PlanEntry{slot++, b, q, std::min(q + DCHUNK, q1)});
+            }
+        }
+        std::vector<PlanEntry> dent;
+        std::vector<int32_t> dptr(nhb + 1, 0);
+        for (int32_t b = 0; b < nhb; ++b) {
+            dent.insert(dent.end(), dl[b].begin(), dl[b].end());
+            dptr[b + 1] = (int32_t)dent.size();
+        }
+        plan.dense_ent.alloc(std::max<size_t>(dent.size(), 1));
+        plan.dense_ptr.alloc(nhb + 1);
+        CPD_CUDA(cudaMemcpy(plan.dense_ent.p, dent.data(), sizeof(PlanEntry) * dent.size(), cudaMemcpyHostToDevice));
+        CPD_CUDA(cudaMemcpy(plan.dense_ptr.p, dptr.data(), sizeof(int32_t) * (nhb + 1), cudaMemcpyHostToDevice));
+    }
     std::vector<int32_t> next(lptr.begin(), lptr.end() - 1), lents;
     int64_t npieces = 0;
     plan.seg.assign(1, 0);
@@ -128,7 +186,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     plan.nlong = nl;
     plan.rows_entries = nrows_e;
     plan.single_entries = nsingle;
-    plan.long_pieces = npieces;
+    plan.long_pieces = (int64_t)lptr[nl];
     (void)lents;
     plan.nslab = nslab;
     plan.ent.alloc(std::max<size_t>(ent.size(), 1));
@@ -498,8 +556,16 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         CPD_CUDA(cudaMemcpy(hp.data(), P->A.p.p, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
         CPD_CUDA(cudaMemcpy(htp.data(), P->AT.p.p, sizeof(int32_t) * htp.size(), cudaMemcpyDeviceToHost));
         // A: warp-item plan for k_csrw unless CPD_WARP=0 (then the TMA plan of k_spmv)
+        // default: warp plan when rows longer than WLONG carry >= 25% of the nonzeros
+        // (C3, C5: measured faster); short-row matrices keep the TMA plan (C2, C4)
         const char* we = getenv("CPD_WARP");
-        const bool warpA = !(we && we[0] == '0');
+        int64_t long_nnz = 0;
+        for (int32_t r = 0; r < m; ++r) {
+            const int64_t len = (int64_t)hp[r + 1] - hp[r];
+            if (len > WLONG) long_nnz += len;
+        }
+        bool warpA = 4 * long_nnz >= nnz && nnz > 0;
+        if (we) warpA = we[0] != '0';
         build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.plan, warpA);
         build_plan(n, m, htp, P->AT.p.p, P->AT.j.p, P->AT.plan);
         // SELL-32 where the rows are short and even (padding <= 25%); CPD_SELL=0 disables

@@ -72,15 +72,15 @@ Ctx::~Ctx()
 DevPlan Ctx::planA() const
 {
     const Plan& pl = P->A.plan;
-    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p,
-                   lpartA.p};
+    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
+                   pl.dense_ptr.p, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p, lpartA.p};
 }
 
 DevPlan Ctx::planAT() const
 {
     const Plan& pl = P->AT.plan;
-    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p,
-                   lpartAT.p};
+    return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
+                   pl.dense_ptr.p, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p, lpartAT.p};
 }
 
 void Ctx::pull_ctl()
@@ -148,6 +148,27 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
                 wsms = cx.P->num_sms;
                 wgrid = std::max(1, nb) * wsms;
             }
+        }
+        Gate g0 = g;
+        g0.active = nullptr;
+        if (dp.nheavy > 0) {   // heavy rows by dense column blocks (their slots, then k_finish)
+            constexpr size_t DSM = (size_t)NV * HB * sizeof(double);
+            static int dgrid = 0, dsms = 0;
+            {
+                std::lock_guard<std::mutex> lk(g_grid_mu);
+                if (!dgrid || dsms != cx.P->num_sms) {
+                    CPD_CUDA(cudaFuncSetAttribute(k_dense<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)DSM));
+                    int nb = 0;
+                    CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dense<NV>, TPB_D, DSM));
+                    dsms = cx.P->num_sms;
+                    dgrid = std::max(1, nb) * dsms;
+                }
+            }
+            const int grd = std::max(1, std::min(dgrid, dp.nhb));
+            k_dense<NV><<<grd, TPB_D, DSM, cx.st>>>(M.dev(), dp, M.cols, v0, v1, g0, cx.ctl);
+            CPD_CUDA(cudaGetLastError());
+            ++cx.launches;
         }
         // one launch per item segment (rows items, then each column slab's pieces), so
         // all warps sweep one slab of the gathered vector at a time (L2-resident)

@@ -275,3 +275,25 @@ def test_trajectory(problems):
     k, off, rp = S.trajectory()
     assert len(k) == r["iterations"] // 64
     assert np.all(np.diff(k) == 64) and np.all(off >= 0) and np.all(rp >= 0)
+
+
+@pytest.mark.parametrize("fmt", [("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")])
+@pytest.mark.parametrize("name", ["c1", "c2-s", "c3-s", "c4-s", "c5-s"])
+def test_every_spmv_format_lockstep(name, fmt, monkeypatch):
+    """Each SpMV engine (TMA plan k_spmv / warp-item k_csrw for A; SELL-32 k_sell or
+    the TMA plan for A^T) meets the 1e-9 iterate contract, restarts on."""
+    warp, sell = fmt
+    monkeypatch.setenv("CPD_WARP", warp)
+    monkeypatch.setenv("CPD_SELL", sell)
+    lp = lpgen.config(name)
+    olp = oracle.OracleLP(lp)
+    P = cpd.Problem.from_lp(lp)
+    eta = 0.9 / oracle.power_sigma(olp)
+    S = cpd.Solver(P, step_size=eta, restart=1)
+    R = oracle.Run(olp, oracle.default_params(step_size=eta, restart=1), mode=oracle.MODE_NONE)
+    S.step(300)
+    R.run(300)
+    xg, yg = S.get_iterate()
+    xo, yo = R.get()
+    assert close(xg, xo) and close(yg, yo), (name, fmt)
+    assert P.power_sigma(128, 7) == pytest.approx(oracle.power_sigma(olp, 128, 7), rel=1e-12)

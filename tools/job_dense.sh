@@ -1,0 +1,6 @@
+set -x
+OUT=gpurun_out/r1s2h; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || exit 1
+timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; tail -5 $OUT/pytest_gpu.log
+timeout 600 python tools/kern_time.py --config c5 --corner 1 2>&1 | tee $OUT/kt_c5.txt
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct --clock-control none --kernel-name-base demangled -k "regex:k_csrw|k_finish|k_sell" -s 10 -c 14 python tools/prof_run.py --iters 3 > $OUT/ncu_seg.log 2>&1; grep -E "^  void|duration|bytes" $OUT/ncu_seg.log | tail -40
