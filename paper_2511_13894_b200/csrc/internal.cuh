@@ -70,13 +70,18 @@ struct Plan {
     int32_t nheavy = 0, nhb = 0;          // heavy rows (k_dense) and column blocks of HB
     DBuf<PlanEntry> dense_ent;            // {slot, block, q0, q1} grouped by block
     DBuf<int32_t> dense_ptr;              // [nhb + 1] item range of each block
+    // short rows by column slab (k_short): [nslab][rows + 1] pointers, entries slab-major
+    int32_t short_on = 0;
+    int64_t short_nnz = 0;
+    DBuf<int32_t> short_ptr, short_col;
+    DBuf<double> short_val;
     int64_t rows_entries = 0, single_entries = 0, long_pieces = 0;
     int32_t nslab = 1;
 };
 // rows x cols CSR with device column array d_col; long rows are cut into CAP pieces
 // at column-slab boundaries and their pieces ordered slab-major.
 void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rowptr, const int32_t* d_p,
-                const int32_t* d_col, Plan& plan, bool warp = false);
+                const int32_t* d_col, const double* d_val, Plan& plan, bool warp = false);
 
 // SELL-32 copy of a CSR layout whose rows are short and of similar length
 // (DESIGN.md §6): slices of 32 consecutive rows, each padded to its longest row,
@@ -159,6 +164,7 @@ struct Ctx {
     DBuf<double> bpart;
     DBuf<unsigned> ctr;
     DBuf<double> lpartA, lpartAT;     // long-row piece partials of each layout
+    DBuf<double> shortA, shortAT;     // running row sums of the short-row slab passes
     DBuf<double> red;                 // this rank's totals of the last reduction (distributed)
     DBuf<double> part, recv;          // reduce-scatter send [world][2][L] / receive [2][L] buffers
     int grid_elem = 0;

@@ -36,7 +36,7 @@ constexpr int NSMAX = 12;      // max scalars an epilogue reduces
 constexpr int WCAP_ROWS = 1024;  // k_csrw: nonzeros per rows item (<= 32 rows)
 constexpr int WLONG = 512;       // k_csrw: a longer row is cut into pieces
 #ifndef CPD_WCAP_LONG
-#define CPD_WCAP_LONG 2048
+#define CPD_WCAP_LONG 512
 #endif
 constexpr int WCAP_LONG = CPD_WCAP_LONG;  // k_csrw: nonzeros per long-row piece
 constexpr int HEAVY_MIN = 65536; // k_dense: rows with at least this many nonzeros
@@ -63,6 +63,10 @@ struct DevPlan {
     int32_t nheavy, nhb;       // heavy rows / dense column blocks (k_dense)
     const PlanEntry* dense_ent;   // {slot, block, q0, q1}: <= DCHUNK entries of one heavy row in one block
     const int32_t* dense_ptr;     // [nhb + 1] items of each block
+    const int32_t* short_ptr;     // [nslab][rows + 1] short-row entries by slab (k_short)
+    const int32_t* short_col;
+    const double* short_val;
+    double* short_part;           // [NV][rows] running sums across slab passes
     const int32_t* long_row;   // [nlong] row index of each long row
     const int32_t* long_ptr;   // [nlong + 1] piece slots of each long row (column order)
     const int32_t* long_ents;  // unused (kept for layout stability)
@@ -1083,6 +1087,66 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
                 for (int v = 0; v < NV; ++v) P.lpart[(size_t)E.a * 2 + v] = sm[v];
         }
     }
+}
+
+// ------------------------------------------------------------ short rows by column slab
+// Rows of at most WLONG entries, with their entries copied slab-major: pass s sums
+// each row's slab-s entries (thread = row, consecutive rows' entries adjacent, so
+// the warp's loads are coalesced at line level) gathering only from the L2-resident
+// slab s of the vector, and carries the running sum in short_part; the last pass
+// adds its slab and runs the fused epilogue for every row that is not long
+// (long rows: k_finish).  Fixed order (slab 0 first): deterministic.
+template <int NV, class Epi>
+__global__ void __launch_bounds__(256)
+k_short(DevCsr M, DevPlan P, int32_t slab, int32_t nslab, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl,
+        double* bpart, unsigned* ctr, double* red, int prev, int fin)
+{
+    constexpr int NS = Epi::NS;
+    constexpr int NVEC = Epi::NVEC;
+    __shared__ int s_go;
+    if (threadIdx.x == 0) {
+        s_go = gate_open(gate, ctl);
+        if (s_go && gate.active && blockIdx.x == 0) gate.active[gate.node] = 1;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    Epi e = epi;
+    e.load(ctl);
+    const double* vin[NVEC > 0 ? NVEC : 1];
+#pragma unroll
+    for (int v = 0; v < NVEC; ++v) vin[v] = e.vec(v);
+    const double* __restrict__ v0 = vs0.get(ctl);
+    const double* __restrict__ v1 = vs1.get(ctl);
+    double acc[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+    const int32_t rows = M.rows;
+    const bool last = slab == nslab - 1;
+    const int32_t* sp = P.short_ptr + (int64_t)slab * (rows + 1);
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t q0 = sp[r], q1 = sp[r + 1];
+        double sm[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sm[v] = slab == 0 ? 0.0 : P.short_part[v * (int64_t)rows + r];
+#pragma unroll 4
+        for (int32_t q = q0; q < q1; ++q) {
+            const int32_t c = __ldcs(P.short_col + q);
+            const double a = __ldcs(P.short_val + q);
+            sm[0] += a * __ldg(&v0[c]);
+            if (NV > 1) sm[NV - 1] += a * __ldg(&v1[c]);
+        }
+        if (!last) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) P.short_part[v * (int64_t)rows + r] = sm[v];
+        } else if (M.p[r + 1] - M.p[r] <= WLONG) {
+            e.row((int)r, sm, vin, (int)r, acc);
+        }
+    }
+    if (!last) return;
+    if (fin)
+        grid_finalize<NS, 256>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+    else
+        block_partial<NS, 256>(acc, bpart, prev);
 }
 
 // Elementwise pass over [0, N) with reductions and a device-side finalize.

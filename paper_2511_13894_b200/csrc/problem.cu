@@ -38,13 +38,46 @@ __global__ void k_slab_pos(int32_t nl, int32_t nb, const int32_t* lrows, const i
     }
 }
 
+// Short rows (<= long_min entries) split by column slab: cnt[s * rows + r] = entries of
+// row r in slab s (0 for long rows).
+__global__ void k_short_count(int32_t rows, int32_t nslab, int64_t long_min, const int32_t* p, const int32_t* col,
+                              int32_t* cnt)
+{
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t a = p[r], b = p[r + 1];
+        for (int32_t s = 0; s < nslab; ++s) cnt[(int64_t)s * rows + r] = 0;
+        if (b - a > long_min) continue;
+        for (int32_t q = a; q < b; ++q) cnt[(int64_t)(col[q] / SLAB_COLS) * rows + r] += 1;
+    }
+}
+
+// entries copied slab-major (row order, then column order inside each slab)
+__global__ void k_short_fill(int32_t rows, int32_t nslab, int64_t long_min, const int32_t* p, const int32_t* col,
+                             const double* val, const int32_t* sp, int32_t* scol, double* sval)
+{
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t a = p[r], b = p[r + 1];
+        if (b - a > long_min) continue;
+        int32_t q = a;
+        for (int32_t s = 0; s < nslab; ++s) {
+            int32_t d = sp[(int64_t)s * (rows + 1) + r];
+            while (q < b && col[q] / SLAB_COLS == s) {
+                scol[d] = col[q];
+                sval[d] = val[q];
+                ++d;
+                ++q;
+            }
+        }
+    }
+}
+
 // Rows entries: maximal runs of consecutive rows with <= CAP nonzeros and <= RMAX
 // rows.  A row with more than SINGLE_MIN nonzeros is LONG: cut at column-slab
 // boundaries and into CAP pieces, pieces ordered slab-major after all rows entries
 // (while the CTAs sweep one slab, that slab of the gathered vector stays in L2);
 // k_finish sums its pieces and applies its epilogue.
 void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, const int32_t* d_p,
-                const int32_t* d_col, Plan& plan, bool warp)
+                const int32_t* d_col, const double* d_val, Plan& plan, bool warp)
 {
     // TMA plan: <= RMAX rows / CAP nnz per entry, rows > SINGLE_MIN long, CAP pieces.
     // warp plan (k_csrw): <= 32 rows / WCAP_ROWS nnz per item, rows > WLONG long, WCAP_LONG pieces.
@@ -174,7 +207,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     plan.seg.assign(1, 0);
     plan.seg.push_back((int32_t)ent.size());
     for (int32_t s = 0; s < nslab; ++s) {
-        if (!by_slab[s].empty()) plan.seg.push_back((int32_t)(ent.size() + by_slab[s].size()));
+        plan.seg.push_back((int32_t)(ent.size() + by_slab[s].size()));   // seg[s + 1 .. s + 2) = slab s
         for (PlanEntry E : by_slab[s]) {
             E.a = next[-1 - E.b]++;   // slab-major visit == column order within each row
             ent.push_back(E);
@@ -189,6 +222,42 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     plan.long_pieces = (int64_t)lptr[nl];
     (void)lents;
     plan.nslab = nslab;
+    // warp plan with >= 2 slabs: short rows also by slab (k_short), so their gathers of
+    // the vector hit the L2-resident slab instead of DRAM
+    plan.short_on = 0;
+    if (warp && nslab >= 2 && rows > 0) {
+        DBuf<int32_t> cnt((size_t)nslab * rows);
+        const int g = (int)std::min<int64_t>(((int64_t)rows + 255) / 256, 8192);
+        k_short_count<<<g, 256>>>(rows, nslab, long_min, d_p, d_col, cnt.p);
+        CPD_CUDA(cudaGetLastError());
+        // sp[s][r] = exclusive prefix over (s, r) in slab-major order; sp[s][rows] = end of slab s
+        plan.short_ptr.alloc((size_t)nslab * (rows + 1));
+        DBuf<int32_t> flat((size_t)nslab * rows + 1);
+        size_t tb = 0;
+        CPD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, flat.p, (int)((int64_t)nslab * rows)));
+        DBuf<unsigned char> tmp(tb);
+        CPD_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, flat.p, (int)((int64_t)nslab * rows)));
+        std::vector<int32_t> hflat((size_t)nslab * rows), hcnt_last(1);
+        CPD_CUDA(cudaMemcpy(hflat.data(), flat.p, sizeof(int32_t) * hflat.size(), cudaMemcpyDeviceToHost));
+        CPD_CUDA(cudaMemcpy(hcnt_last.data(), cnt.p + (size_t)nslab * rows - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        const int64_t total = (int64_t)hflat.back() + hcnt_last[0];
+        std::vector<int32_t> hsp((size_t)nslab * (rows + 1));
+        for (int32_t s2 = 0; s2 < nslab; ++s2) {
+            std::copy(hflat.begin() + (size_t)s2 * rows, hflat.begin() + (size_t)(s2 + 1) * rows,
+                      hsp.begin() + (size_t)s2 * (rows + 1));
+            hsp[(size_t)s2 * (rows + 1) + rows] =
+                (s2 + 1 < nslab) ? hflat[(size_t)(s2 + 1) * rows] : (int32_t)total;
+        }
+        CPD_CUDA(cudaMemcpy(plan.short_ptr.p, hsp.data(), sizeof(int32_t) * hsp.size(), cudaMemcpyHostToDevice));
+        plan.short_col.alloc(std::max<int64_t>(total, 1));
+        plan.short_val.alloc(std::max<int64_t>(total, 1));
+        k_short_fill<<<g, 256>>>(rows, nslab, long_min, d_p, d_col, d_val, plan.short_ptr.p, plan.short_col.p,
+                                 plan.short_val.p);
+        CPD_CUDA(cudaGetLastError());
+        CPD_CUDA(cudaDeviceSynchronize());
+        plan.short_nnz = total;
+        plan.short_on = 1;
+    }
     plan.ent.alloc(std::max<size_t>(ent.size(), 1));
     CPD_CUDA(cudaMemcpy(plan.ent.p, ent.data(), sizeof(PlanEntry) * ent.size(), cudaMemcpyHostToDevice));
     plan.long_row.alloc(std::max(nl, 1));
@@ -566,8 +635,8 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         }
         bool warpA = 4 * long_nnz >= nnz && nnz > 0;
         if (we) warpA = we[0] != '0';
-        build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.plan, warpA);
-        build_plan(n, m, htp, P->AT.p.p, P->AT.j.p, P->AT.plan);
+        build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.x.p, P->A.plan, warpA);
+        build_plan(n, m, htp, P->AT.p.p, P->AT.j.p, P->AT.x.p, P->AT.plan);
         // SELL-32 where the rows are short and even (padding <= 25%); CPD_SELL=0 disables
         const char* se = getenv("CPD_SELL");
         const bool sell_ok = !(se && se[0] == '0');

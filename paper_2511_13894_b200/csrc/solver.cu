@@ -51,6 +51,8 @@ Ctx::Ctx(const cpd_problem* p) : P(p)
     const Plan& pt = p->AT.plan;
     lpartA.alloc((size_t)std::max<int64_t>(1, pa.long_pieces) * GW * 2);
     lpartAT.alloc((size_t)std::max<int64_t>(1, pt.long_pieces) * GW * 2);
+    if (pa.short_on) shortA.alloc((size_t)2 * p->A.rows);
+    if (pt.short_on) shortAT.alloc((size_t)2 * p->AT.rows);
     red.alloc(NSMAX);
     CPD_CUDA(cudaMemset(red.p, 0, sizeof(double) * NSMAX));
     if (p->split >= 0) {
@@ -73,14 +75,16 @@ DevPlan Ctx::planA() const
 {
     const Plan& pl = P->A.plan;
     return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
-                   pl.dense_ptr.p, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p, lpartA.p};
+                   pl.dense_ptr.p, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortA.p, pl.long_row.p,
+                   pl.long_ptr.p, pl.long_ents.p, lpartA.p};
 }
 
 DevPlan Ctx::planAT() const
 {
     const Plan& pl = P->AT.plan;
     return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
-                   pl.dense_ptr.p, pl.long_row.p, pl.long_ptr.p, pl.long_ents.p, lpartAT.p};
+                   pl.dense_ptr.p, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortAT.p, pl.long_row.p,
+                   pl.long_ptr.p, pl.long_ents.p, lpartAT.p};
 }
 
 void Ctx::pull_ctl()
@@ -176,20 +180,39 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         const bool single = dp.nlong == 0;
         int prev = 0;
         Gate gs = g;
-        for (size_t k = 0; k + 1 < seg.size() || (k == 0 && seg.size() < 2); ++k) {
+        auto launch_items = [&](int a, int b, int fin) {
             DevPlan ds = dp;
-            const int a = seg.size() >= 2 ? seg[k] : 0, b = seg.size() >= 2 ? seg[k + 1] : dp.nent;
-            if (b <= a && !single) continue;
             ds.ent = dp.ent + a;
             ds.nent = b - a;
             const int gr = std::max(1, std::min<int>(wgrid, (ds.nent + 7) / 8));
             k_csrw<NV, Epi><<<gr, TPB_W, 0, cx.st>>>(M.dev(), ds, v0, v1, epi, gs, cx.ctl, cx.bpart.p, cx.ctr.p,
-                                                     red, prev, single ? 1 : 0);
+                                                     red, prev, fin);
             CPD_CUDA(cudaGetLastError());
             ++cx.launches;
             gs.active = nullptr;
             prev += gr;
-            if (single) break;
+        };
+        if (M.plan.short_on) {
+            // per slab: the short rows' slab pass, then the slab's long pieces
+            const int nsl = M.plan.nslab;
+            for (int sl = 0; sl < nsl; ++sl) {
+                const int grs = std::max(1, std::min<int>(cx.P->num_sms * 8, (M.rows + 255) / 256));
+                const bool lastp = sl == nsl - 1;
+                k_short<NV, Epi><<<grs, 256, 0, cx.st>>>(M.dev(), dp, sl, nsl, v0, v1, epi, gs, cx.ctl, cx.bpart.p,
+                                                         cx.ctr.p, red, prev, (lastp && single) ? 1 : 0);
+                CPD_CUDA(cudaGetLastError());
+                ++cx.launches;
+                gs.active = nullptr;
+                if (lastp) prev += grs;
+                if (!single && (size_t)sl + 2 < seg.size() && seg[sl + 2] > seg[sl + 1])
+                    launch_items(seg[sl + 1], seg[sl + 2], 0);
+            }
+        } else {
+            for (size_t k = 0; k + 1 < seg.size(); ++k) {
+                if (seg[k + 1] <= seg[k] && !single) continue;
+                launch_items(seg[k], seg[k + 1], single ? 1 : 0);
+                if (single) break;
+            }
         }
         if (dp.nlong > 0) {
             const int gf = std::max(1, std::min(cx.P->num_sms * 8, dp.nlong));

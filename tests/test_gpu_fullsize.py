@@ -1,0 +1,59 @@
+"""Parity at BASELINE.json's FULL sizes, in the configuration bench.py times
+(CUDA-graph batches, default plans/engines) — `-m gpu`.
+
+C3 (4e6 columns), C4 (2e6 columns, 0.54e6 rows) and C5 (2e7 columns, 2.4e8
+nonzeros, Zipf rows: TMA/SELL/warp/dense engines all active) are run from a
+seeded non-trivial warm start for a few lockstep iterations with the restart
+check every 2 iterations (check / restart / average paths exercised), then
+compared with the oracle element by element at the 1e-9 contract
+(BASELINE.json north_star); the corner statistics of the final iterate are
+recounted by the oracle bit-exactly.  The oracle needs ~4 s per C5 iteration on
+one core, so the C5 leg is a handful of iterations.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import lpgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2511_13894_b200 as cpd  # noqa: E402
+
+
+def close(a, b, rtol=1e-9):
+    return np.linalg.norm(a - b) <= rtol * np.linalg.norm(b) + 1e-14 * math.sqrt(b.size)
+
+
+@pytest.mark.parametrize("name,iters", [("c3", 6), ("c4", 6), ("c5", 4)])
+def test_fullsize_lockstep(name, iters):
+    lp = lpgen.config(name)
+    olp = oracle.OracleLP(lp)
+    rng = np.random.default_rng(123)
+    x0 = np.minimum(np.maximum(rng.uniform(-1.0, 5.0, lp.n), lp.lb), lp.ub)
+    y0 = rng.standard_normal(lp.m)
+    eta = 0.9 / oracle.power_sigma(olp, 4, 7)       # explicit step (S-2): any fixed eta
+    prm = dict(step_size=eta, restart=1, check_every=2)
+    P = cpd.Problem.from_lp(lp)
+    S = cpd.Solver(P, **prm)
+    S.set_iterate(x0, y0)
+    S.step(iters)
+    R = oracle.Run(olp, oracle.default_params(**prm), x_init=x0, y_init=y0, mode=oracle.MODE_NONE)
+    R.run(iters)
+    xg, yg = S.get_iterate()
+    xo, yo = R.get()
+    assert close(xg, xo), (name, np.abs(xg - xo).max())
+    assert close(yg, yo), (name, np.abs(yg - yo).max())
+    # corner counts of the identical (x, z) at full size: bit-exact
+    xg2, yg2, zg = S.get_iterate(z=True)
+    st = P.stats(xg2, zg, eps_abs=1e-6, floor=100_000)
+    ref = oracle.stats(lp.m, xg2, zg, lp.lb, lp.ub, None, None, 1e-6, 100_000)
+    for k in ("off_bound", "off_bound_strict", "zero_rc", "candidates", "est_primal_pushes",
+              "est_dual_pushes", "is_candidate"):
+        assert st[k] == ref[k], k
