@@ -224,8 +224,11 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     plan.nslab = nslab;
     // warp plan with >= 2 slabs: short rows also by slab (k_short), so their gathers of
     // the vector hit the L2-resident slab instead of DRAM
+    // Off by default: measured slower on C5 (5 latency-bound passes of ~210 us vs one
+    // 453 us rows segment, profiles/r01_kernel_iterations.md v18); CPD_SHORT=1 enables.
     plan.short_on = 0;
-    if (warp && nslab >= 2 && rows > 0) {
+    const char* she = getenv("CPD_SHORT");
+    if (warp && nslab >= 2 && rows > 0 && she && she[0] == '1') {
         DBuf<int32_t> cnt((size_t)nslab * rows);
         const int g = (int)std::min<int64_t>(((int64_t)rows + 255) / 256, 8192);
         k_short_count<<<g, 256>>>(rows, nslab, long_min, d_p, d_col, cnt.p);

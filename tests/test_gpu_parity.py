@@ -277,14 +277,17 @@ def test_trajectory(problems):
     assert np.all(np.diff(k) == 64) and np.all(off >= 0) and np.all(rp >= 0)
 
 
-@pytest.mark.parametrize("fmt", [("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")])
+@pytest.mark.parametrize("fmt", [("0", "0", "0"), ("1", "0", "0"), ("0", "1", "0"), ("1", "1", "0"),
+                                 ("1", "1", "1")])
 @pytest.mark.parametrize("name", ["c1", "c2-s", "c3-s", "c4-s", "c5-s"])
 def test_every_spmv_format_lockstep(name, fmt, monkeypatch):
-    """Each SpMV engine (TMA plan k_spmv / warp-item k_csrw for A; SELL-32 k_sell or
-    the TMA plan for A^T) meets the 1e-9 iterate contract, restarts on."""
-    warp, sell = fmt
+    """Each SpMV engine (TMA plan k_spmv / warp-item k_csrw (+ k_dense heavy rows,
+    + k_short slab passes) for A; SELL-32 k_sell or the TMA plan for A^T) meets the
+    1e-9 iterate contract, restarts on."""
+    warp, sell, short = fmt
     monkeypatch.setenv("CPD_WARP", warp)
     monkeypatch.setenv("CPD_SELL", sell)
+    monkeypatch.setenv("CPD_SHORT", short)
     lp = lpgen.config(name)
     olp = oracle.OracleLP(lp)
     P = cpd.Problem.from_lp(lp)
