@@ -115,6 +115,8 @@ def lib():
                                            C.POINTER(C.c_int64)]
             L.orc_stats.argtypes = [C.c_int32, C.c_int32, P, P, P, P, P, P, C.c_double,
                                     C.c_int64, C.POINTER(Stats)]
+            L.orc_scale.argtypes = [C.c_int32, C.c_int32, P, P, P, C.c_int32, C.c_int32, P, P]
+            L.orc_set_original.argtypes = [P, C.POINTER(LPStruct), P, P, P, P, P]
             _lib = L
     return _lib
 
@@ -212,6 +214,12 @@ class Run:
         self.h = lib().orc_create(C.byref(olp.s), C.byref(params), _p(cc), _p(ll), _p(uu),
                                   _p(xi), _p(yi), mode, target, min_iters, eta)
 
+    def set_original(self, olp: "OracleLP", c, lb, ub, r, s):
+        """This run is the scaled image of `olp` (orc_set_original): scores on the original."""
+        keep = [_f64(c), _f64(lb), _f64(ub), _f64(r), _f64(s)]
+        self._keep += keep + [olp]
+        lib().orc_set_original(self.h, C.byref(olp.s), *[_p(a) for a in keep])
+
     def run(self, steps) -> int:
         return int(lib().orc_run(self.h, steps))
 
@@ -243,6 +251,72 @@ class Run:
         if h:
             lib().orc_destroy(h)
             self.h = None
+
+
+class ScaledLP:
+    """Diagonal preconditioning of an LP (orc_scale, R-3):
+    `olp` = the scaled LP  A^ = diag(r) A diag(s), b^ = r b, c^ = s c, l^ = l / s, u^ = u / s,
+    with x = s x^, y = r y^, z = z^ / s."""
+
+    def __init__(self, olp: OracleLP, ruiz_iters=10, pc=1):
+        import types
+        m, n = olp.m, olp.n
+        Ax = olp.Ax.copy()
+        self.r = np.zeros(m)
+        self.s = np.zeros(n)
+        lib().orc_scale(m, n, _p(olp.Ap), _p(olp.Aj), _p(Ax), int(ruiz_iters), int(pc), _p(self.r), _p(self.s))
+        nnz = int(olp.Ap[-1])
+        tp = np.zeros(n + 1, np.int32)
+        tj = np.zeros(max(nnz, 1), np.int32)
+        tx = np.zeros(max(nnz, 1))
+        lib().orc_transpose(m, n, _p(olp.Ap), _p(olp.Aj), _p(Ax), _p(tp), _p(tj), _p(tx))
+        ns = types.SimpleNamespace(m=m, n=n, ATp=tp, ATj=tj[:nnz], ATx=tx[:nnz], b=self.r * olp.b,
+                                   c=self.s * olp.c, lb=olp.lb / self.s, ub=olp.ub / self.s)
+        self.olp = OracleLP(ns)
+        self.orig = olp
+
+
+def solve_scaled(olp: OracleLP, params: Params = None, ruiz_iters=10, pc=1, x_init=None, y_init=None):
+    """Phase 1 on the diagonally scaled LP, terminated by the ORIGINAL LP's criteria
+    (P:119-131); returns the unscaled (x, y, result) and the ScaledLP."""
+    params = params or default_params()
+    sl = ScaledLP(olp, ruiz_iters, pc)
+    xi = None if x_init is None else _f64(x_init) / sl.s
+    yi = None if y_init is None else _f64(y_init) / sl.r
+    r = Run(sl.olp, params, x_init=xi, y_init=yi)
+    r.set_original(olp, olp.c, olp.lb, olp.ub, sl.r, sl.s)
+    r.run(np.iinfo(np.int64).max)
+    xh, yh = r.get()
+    return sl.s * xh, sl.r * yh, r.result(), sl
+
+
+def corner_push_scaled(olp: OracleLP, sl: "ScaledLP", x, y, params: Params = None, eps_abs=1e-6,
+                       obj_scale=1.0, seed=1001, obj=None, min_iters=100, max_iters=100000, eta=0.0,
+                       floor=100_000):
+    """Algorithm 1 in the original space (z = c - A^T y, bound map, Uniform objective),
+    steering iterations on the scaled corner model (c^ s, l^ / s, u^ / s) from x / s, y = 0,
+    stopped by the ORIGINAL ||b - A x||.  Returns as corner_push."""
+    params = params or default_params()
+    z = reduced_costs(olp, y)
+    lh, uh, ch, fl, fu = corner_model(olp, x, z, eps_abs, obj_scale, seed)
+    if obj is not None:
+        ch = _f64(obj)
+    before = stats(olp.m, x, z, olp.lb, olp.ub, lh, uh, eps_abs, floor)
+    p2 = default_params(**{k: getattr(params, k) for k, _ in Params._fields_})
+    p2.max_iters = max_iters
+    p2.primal_weight = 0.0
+    target = params.eps_rel * (1.0 + olp.nb)
+    r = Run(sl.olp, p2, c=sl.s * ch, lb=lh / sl.s, ub=uh / sl.s, x_init=_f64(x) / sl.s, y_init=None,
+            mode=MODE_PRIMAL_ONLY, target=target, min_iters=min_iters, eta=eta)
+    r.set_original(olp, ch, lh, uh, sl.r, sl.s)
+    r.run(np.iinfo(np.int64).max)
+    xh, _ = r.get()
+    xh = sl.s * xh
+    res = r.result()
+    after = stats(olp.m, xh, z, olp.lb, olp.ub, lh, uh, eps_abs, floor)
+    before["fix_lb"] = after["fix_lb"] = fl
+    before["fix_ub"] = after["fix_ub"] = fu
+    return xh, y, z, res, before, after, dict(lhat=lh, uhat=uh, chat=ch, target=target)
 
 
 def solve(olp: OracleLP, params: Params = None, **kw):

@@ -212,6 +212,49 @@ double orc_power_sigma(const orc_lp *lp, int32_t iters, uint64_t seed)
     return sqrt(nu);
 }
 
+/* ------------------------------------------------ diagonal preconditioning */
+
+/* Ruiz + Pock-Chambolle scaling of A (the cuPDLP+ lineage the
+ * paper's PDHG follows; reading R-3).  On CSR(A) (m rows)
+ * in place, r (m) and s (n) start at 1:
+ *   Ruiz, `ruiz_iters` passes:  rho_i = sqrt(max_j |a_ij|), kappa_j = sqrt(max_i |a_ij|)
+ *   then, if pc, one Pock-Chambolle (alpha = 1) pass:
+ *                               rho_i = sqrt(sum_j |a_ij|),  kappa_j = sqrt(sum_i |a_ij|)
+ *   each pass (a zero row/column gets 1):  a_ij <- a_ij / (rho_i kappa_j),
+ *                                          r_i <- r_i / rho_i,  s_j <- s_j / kappa_j
+ * so that the scaled matrix is diag(r) A diag(s). */
+void orc_scale(int32_t m, int32_t n, const int32_t *Ap, const int32_t *Aj, double *Ax,
+               int32_t ruiz_iters, int32_t pc, double *r, double *s)
+{
+    double *rho = (double *)malloc(sizeof(double) * (m ? m : 1));
+    double *kap = (double *)malloc(sizeof(double) * (n ? n : 1));
+    for (int32_t i = 0; i < m; ++i) r[i] = 1.0;
+    for (int32_t j = 0; j < n; ++j) s[j] = 1.0;
+    for (int32_t pass = 0; pass < ruiz_iters + (pc ? 1 : 0); ++pass) {
+        int sum = pass >= ruiz_iters;   /* the Pock-Chambolle pass */
+        for (int32_t i = 0; i < m; ++i) rho[i] = 0.0;
+        for (int32_t j = 0; j < n; ++j) kap[j] = 0.0;
+        for (int32_t i = 0; i < m; ++i)
+            for (int64_t k = Ap[i]; k < Ap[i + 1]; ++k) {
+                double a = fabs(Ax[k]);
+                int32_t j = Aj[k];
+                if (sum) { rho[i] += a; kap[j] += a; }
+                else {
+                    if (a > rho[i]) rho[i] = a;
+                    if (a > kap[j]) kap[j] = a;
+                }
+            }
+        for (int32_t i = 0; i < m; ++i) rho[i] = rho[i] > 0.0 ? sqrt(rho[i]) : 1.0;
+        for (int32_t j = 0; j < n; ++j) kap[j] = kap[j] > 0.0 ? sqrt(kap[j]) : 1.0;
+        for (int32_t i = 0; i < m; ++i)
+            for (int64_t k = Ap[i]; k < Ap[i + 1]; ++k) Ax[k] = Ax[k] / (rho[i] * kap[Aj[k]]);
+        for (int32_t i = 0; i < m; ++i) r[i] = r[i] / rho[i];
+        for (int32_t j = 0; j < n; ++j) s[j] = s[j] / kap[j];
+    }
+    free(rho);
+    free(kap);
+}
+
 /* ------------------------------------------------------------------ R-PDHG */
 typedef struct {
     const orc_lp *lp;
@@ -226,6 +269,12 @@ typedef struct {
     double S_r, S_prev;
     int status, returned_average;
     double t0;
+    /* scaled run (orc_set_original): score and primal residual on the ORIGINAL LP at
+     * the unscaled point x = s x^, y = r y^ (P:119-131 are criteria of the LP as given) */
+    const orc_lp *orig;
+    const double *oc, *ol, *ou, *sr, *sc;
+    double onb, onc;
+    double *ux, *uy;
 } orc_state;
 
 void orc_destroy(orc_state *s)
@@ -233,11 +282,18 @@ void orc_destroy(orc_state *s)
     if (!s) return;
     free(s->x); free(s->y); free(s->xavg); free(s->yavg); free(s->xr); free(s->yr);
     free(s->xn); free(s->yn); free(s->aty); free(s->xbar); free(s->axbar);
+    free(s->ux); free(s->uy);
     free(s);
 }
 
 static double score_of(orc_state *s, const double *x, const double *y, orc_score_t *o)
 {
+    if (s->orig) {
+        for (int32_t j = 0; j < s->lp->n; ++j) s->ux[j] = s->sc[j] * x[j];
+        for (int32_t i = 0; i < s->lp->m; ++i) s->uy[i] = s->sr[i] * y[i];
+        orc_score(s->orig, s->oc, s->ol, s->ou, s->onb, s->onc, s->ux, s->uy, o);
+        return o->score;
+    }
     orc_score(s->lp, s->c, s->l, s->u, s->nb, s->nc, x, y, o);
     return o->score;
 }
@@ -292,9 +348,32 @@ double orc_get_eta(const orc_state *s) { return s->eta; }
 double orc_get_omega(const orc_state *s) { return s->omega; }
 int64_t orc_get_k(const orc_state *s) { return s->k; }
 
+/* Mark a run as the scaled image of `orig` (objective oc, bounds ol/ou in original
+ * space, x = sc x^, y = sr y^): termination, restart scores and the primal-only
+ * residual are then evaluated on the original LP; everything else (steps, primal
+ * weight, restart distances) stays in the scaled space.  Re-scores the start. */
+void orc_set_original(orc_state *s, const orc_lp *orig, const double *oc, const double *ol,
+                      const double *ou, const double *sr, const double *sc)
+{
+    s->orig = orig; s->oc = oc; s->ol = ol; s->ou = ou; s->sr = sr; s->sc = sc;
+    s->onb = orc_norm2(orig->m, orig->b);
+    s->onc = orc_norm2(orig->n, oc);
+    s->ux = (double *)calloc((size_t)(s->lp->n ? s->lp->n : 1), 8);
+    s->uy = (double *)calloc((size_t)(s->lp->m ? s->lp->m : 1), 8);
+    orc_score_t o;
+    s->S_r = score_of(s, s->x, s->y, &o);
+    s->status = -1;
+    if (s->mode == MODE_FULL && s->S_r <= s->prm.eps_rel) s->status = 0;
+}
+
 static double primal_res(orc_state *s, const double *x)
 {
     const orc_lp *lp = s->lp;
+    if (s->orig) {   /* ||b - A x|| of the original LP at x = s x^ */
+        for (int32_t j = 0; j < lp->n; ++j) s->ux[j] = s->sc[j] * x[j];
+        lp = s->orig;
+        x = s->ux;
+    }
     orc_spmv(lp->m, lp->Ap, lp->Aj, lp->Ax, x, s->axbar);
     double r2 = 0.0;
     for (int32_t i = 0; i < lp->m; ++i) {

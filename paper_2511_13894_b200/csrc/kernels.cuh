@@ -170,6 +170,35 @@ __device__ __forceinline__ double u01(uint64_t seed, int64_t j)
     return (double)(s >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// L2 eviction-priority helpers: the primal iterate x+ (gathered by the next dual
+// step) is written / gathered evict-last so it outlives the streamed matrix data
+// in L2 (CPD_XLAST=0 disables, for A/B measurements).
+#ifndef CPD_XLAST
+#define CPD_XLAST 1
+#endif
+__device__ __forceinline__ void st_keep(double* p, double v)
+{
+#if CPD_XLAST
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#else
+    *p = v;
+#endif
+}
+__device__ __forceinline__ double ld_keep(const double* p)
+{
+#if CPD_XLAST
+    uint64_t pol;
+    double v;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 // KKT score terms (S-3): o = {rp, rd, pobj, dobj, r_p, r_d, r_g, score}
 __device__ __forceinline__ void score8(double rp2, double rd2, double pobj, double dobj,
                                        double nb, double nc, double* o)
@@ -705,16 +734,24 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
     double acc[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-    for (int l = blockIdx.x; l < P.nlong; l += gridDim.x) {
+    // one warp per long row: lane-strided partials, xor-reduction (fixed order)
+    (void)s_w;
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (TPB / 32);
+    for (int l = (blockIdx.x * TPB + threadIdx.x) >> 5; l < P.nlong; l += nw) {
         double sm[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) sm[v] = 0.0;
         const int64_t t0 = (int64_t)P.long_ptr[l] * P.pslot, t1 = (int64_t)P.long_ptr[l + 1] * P.pslot;
-        for (int64_t t = t0 + threadIdx.x; t < t1; t += TPB)
+#pragma unroll 4
+        for (int64_t t = t0 + lane; t < t1; t += 32)
 #pragma unroll
             for (int v = 0; v < NV; ++v) sm[v] += __ldcg(&P.lpart[t * 2 + v]);
-        block_sum<NV>(sm, s_w);
-        if (threadIdx.x == 0) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sm[v] += __shfl_xor_sync(0xffffffffu, sm[v], o);
+        if (lane == 0) {
             const int r = P.long_row[l];
             e.row(r, sm, vin, r, acc);
         }
@@ -925,7 +962,7 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
                 double g[WU][NV];
 #pragma unroll
                 for (int u = 0; u < WU; ++u) {
-                    g[u][0] = c[u] >= 0 ? __ldg(&v0[c[u]]) : 0.0;
+                    g[u][0] = c[u] >= 0 ? ld_keep(&v0[c[u]]) : 0.0;
                     if (NV > 1) g[u][NV - 1] = c[u] >= 0 ? __ldg(&v1[c[u]]) : 0.0;
                 }
                 int cn[WU];
@@ -994,7 +1031,7 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
                 double g[WU][NV];
 #pragma unroll
                 for (int u = 0; u < WU; ++u) {
-                    g[u][0] = c[u] >= 0 ? __ldg(&v0[c[u]]) : 0.0;
+                    g[u][0] = c[u] >= 0 ? ld_keep(&v0[c[u]]) : 0.0;
                     if (NV > 1) g[u][NV - 1] = c[u] >= 0 ? __ldg(&v1[c[u]]) : 0.0;
                 }
                 int cn[WU];
@@ -1297,7 +1334,7 @@ struct EpiPrimalT {
             hi = vin[4][li];
         }
         const double xp = proj(x - tau * z, lo, hi);
-        xn[j] = xp;
+        st_keep(&xn[j], xp);
         const double xa = vin[2][li];
         // averages are read once per iteration: streamed (evict-first) so L2 keeps x+
         __stcs(&xan[j], xa + (xp - xa) * inv_t);   // (x+ - x_avg)/t as a multiply (<= 1 ulp)

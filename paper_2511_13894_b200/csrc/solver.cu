@@ -155,31 +155,33 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         }
         Gate g0 = g;
         g0.active = nullptr;
-        if (dp.nheavy > 0) {   // heavy rows by dense column blocks (their slots, then k_finish)
-            constexpr size_t DSM = (size_t)NV * HB * sizeof(double);
-            static int dgrid = 0, dsms = 0;
-            {
-                std::lock_guard<std::mutex> lk(g_grid_mu);
-                if (!dgrid || dsms != cx.P->num_sms) {
-                    CPD_CUDA(cudaFuncSetAttribute(k_dense<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)DSM));
-                    int nb = 0;
-                    CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dense<NV>, TPB_D, DSM));
-                    dsms = cx.P->num_sms;
-                    dgrid = std::max(1, nb) * dsms;
-                }
-            }
-            const int grd = std::max(1, std::min(dgrid, dp.nhb));
-            k_dense<NV><<<grd, TPB_D, DSM, cx.st>>>(M.dev(), dp, M.cols, v0, v1, g0, cx.ctl);
-            CPD_CUDA(cudaGetLastError());
-            ++cx.launches;
-        }
         // one launch per item segment (rows items, then each column slab's pieces), so
         // all warps sweep one slab of the gathered vector at a time (L2-resident)
         const std::vector<int32_t>& seg = M.plan.seg;
         const bool single = dp.nlong == 0;
         int prev = 0;
         Gate gs = g;
+        auto launch_dense = [&]() {
+            if (dp.nheavy > 0) {   // heavy rows by dense column blocks (their slots, then k_finish)
+                constexpr size_t DSM = (size_t)NV * HB * sizeof(double);
+                static int dgrid = 0, dsms = 0;
+                {
+                    std::lock_guard<std::mutex> lk(g_grid_mu);
+                    if (!dgrid || dsms != cx.P->num_sms) {
+                        CPD_CUDA(cudaFuncSetAttribute(k_dense<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      (int)DSM));
+                        int nb = 0;
+                        CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dense<NV>, TPB_D, DSM));
+                        dsms = cx.P->num_sms;
+                        dgrid = std::max(1, nb) * dsms;
+                    }
+                }
+                const int grd = std::max(1, std::min(dgrid, dp.nhb));
+                k_dense<NV><<<grd, TPB_D, DSM, cx.st>>>(M.dev(), dp, M.cols, v0, v1, g0, cx.ctl);
+                CPD_CUDA(cudaGetLastError());
+                ++cx.launches;
+            }
+        };
         auto launch_items = [&](int a, int b, int fin) {
             DevPlan ds = dp;
             ds.ent = dp.ent + a;
@@ -193,6 +195,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
             prev += gr;
         };
         if (M.plan.short_on) {
+            launch_dense();
             // per slab: the short rows' slab pass, then the slab's long pieces
             const int nsl = M.plan.nslab;
             for (int sl = 0; sl < nsl; ++sl) {
@@ -208,14 +211,18 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
                     launch_items(seg[sl + 1], seg[sl + 2], 0);
             }
         } else {
+            // rows items first (x+ just written by the primal step is still in L2), then
+            // the heavy rows' dense blocks, then each slab's long pieces
             for (size_t k = 0; k + 1 < seg.size(); ++k) {
+                if (k == 1) launch_dense();
                 if (seg[k + 1] <= seg[k] && !single) continue;
                 launch_items(seg[k], seg[k + 1], single ? 1 : 0);
                 if (single) break;
             }
+            if (seg.size() < 3) launch_dense();
         }
         if (dp.nlong > 0) {
-            const int gf = std::max(1, std::min(cx.P->num_sms * 8, dp.nlong));
+            const int gf = std::max(1, std::min(cx.P->num_sms * 8, (dp.nlong + TPB / 32 - 1) / (TPB / 32)));
             Gate g2 = g;
             g2.active = nullptr;
             k_finish<NV, Epi><<<gf, TPB, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, prev, red);
@@ -244,7 +251,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
     CPD_CUDA(cudaGetLastError());
     ++cx.launches;
     if (dp.nlong > 0) {
-        const int gf = std::max(1, std::min(cx.P->num_sms * 8, dp.nlong));
+        const int gf = std::max(1, std::min(cx.P->num_sms * 8, (dp.nlong + TPB / 32 - 1) / (TPB / 32)));
         Gate g2 = g;
         g2.active = nullptr;
         k_finish<NV, Epi><<<gf, TPB, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, gr, red);
