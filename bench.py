@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--tte", default="c2,c4", help="configs for the time-to-eps side measurement ('' = off)")
+    ap.add_argument("--tte", default="c2,c3,c4", help="configs for the time-to-eps side measurement ('' = off)")
     ap.add_argument("--ref-iters", type=int, default=0, help="oracle iterations per reference step (0: auto)")
     ap.add_argument("--partition", type=int, default=-1,
                     help="multi-GPU partition: 0 row-block, 1 col-block, -1 auto (shard the long side)")
@@ -230,24 +230,28 @@ def cpu_baseline(lp):
 
 
 def time_to_eps(names, device):
-    """Wall time from cpd_solve entry to return at eps_rel = 1e-4 (problem resident)."""
+    """Wall time from cpd_solve entry to return at eps_rel = 1e-4 (problem resident),
+    plain R-PDHG and with the diagonal preconditioning (cpd_problem_scale, NEXT-1)."""
     import lpgen
     import paper_2511_13894_b200 as cpd
     out = {}
     for nm in names:
         lp = lpgen.config(nm)
-        P = cpd.Problem.from_lp(lp, device=device)
-        S = cpd.Solver(P, max_iters=200000)
-        S.solve()   # warm-up (graph capture)
-        S.set_iterate(None, None)
-        r = S.solve()
-        rc, _, _ = S.corner_push(max_iters=200000)   # Algorithm 1 from the phase-1 point
-        out[nm] = {"status": cpd.STATUS[r["status"]], "iterations": r["iterations"], "seconds": r["wall_s"],
-                   "it_per_s": r["iterations"] / r["wall_s"], "corner_status": cpd.STATUS[rc["status"]],
-                   "corner_iterations": rc["iterations"],
-                   "corner_seconds": rc["wall_s"]}
-        S.close()
-        P.close()
+        for tag, scale in (("", False), (":scaled", True)):
+            P = cpd.Problem.from_lp(lp, device=device)
+            if scale:
+                P.scale(10, 1)
+            S = cpd.Solver(P, max_iters=200000)
+            S.solve()   # warm-up (graph capture)
+            S.set_iterate(None, None)
+            r = S.solve()
+            rc, _, _ = S.corner_push(max_iters=200000)   # Algorithm 1 from the phase-1 point
+            out[nm + tag] = {"status": cpd.STATUS[r["status"]], "iterations": r["iterations"],
+                             "seconds": r["wall_s"], "it_per_s": r["iterations"] / r["wall_s"],
+                             "pobj": r["pobj"], "corner_status": cpd.STATUS[rc["status"]],
+                             "corner_iterations": rc["iterations"], "corner_seconds": rc["wall_s"]}
+            S.close()
+            P.close()
     return out
 
 

@@ -203,6 +203,22 @@ int cpd_solver_counters(const cpd_solver *s, int64_t out[4]);
 /* Algorithmic bytes one launch of kernel `name` moves (DESIGN.md byte model). */
 int cpd_kernel_bytes(const cpd_solver *s, const char *name, double *bytes);
 
+/* ------------------------------------------------------------------ preconditioning
+ * Diagonal scaling of the problem (the cuPDLP+ lineage the
+ * paper's PDHG follows; reading R-3): `ruiz_iters` Ruiz passes
+ * (rho_i = sqrt(max_j |a_ij|), kappa_j = sqrt(max_i |a_ij|)) then, if pock_chambolle,
+ * one Pock-Chambolle alpha = 1 pass (square roots of row / column sums of |a_ij|);
+ * each pass a_ij /= rho_i kappa_j.  The device LP becomes A^ = diag(r) A diag(s),
+ * b^ = r b, c^ = s c, l^ = l / s, u^ = u / s; solvers iterate on it (step size, primal
+ * weight and restart distances in the scaled space) while termination, restart
+ * scores, the steering stop and all statistics are those of the ORIGINAL LP
+ * (P:119-131), and every iterate in or out of the ABI is original-space.
+ * Call once, before creating solvers; single-GPU problems only (CPD_E_ARG otherwise,
+ * CPD_E_STATE if already scaled). */
+int cpd_problem_scale(cpd_problem *p, int32_t ruiz_iters, int32_t pock_chambolle);
+/* The scale vectors r[m], s[n] (host); CPD_E_STATE if the problem is not scaled. */
+int cpd_problem_get_scaling(const cpd_problem *p, double *r, double *s);
+
 /* ------------------------------------------------------------------ multi-GPU
  * One process per GPU.  The LP is split into
  * contiguous blocks balanced by nonzeros (+1 per row for the vector work):

@@ -32,6 +32,7 @@ DECLARED_SYMBOLS = [
     "cpd_get_trajectory", "cpd_power_sigma", "cpd_problem_score", "cpd_compute_stats",
     "cpd_get_kernel_times", "cpd_kernel_bytes", "cpd_solver_counters",
     "cpd_partition", "cpd_nccl_get_unique_id", "cpd_problem_create_dist", "cpd_problem_dist_info",
+    "cpd_problem_scale", "cpd_problem_get_scaling",
 ]
 
 
@@ -116,6 +117,8 @@ def lib():
             "cpd_problem_create_dist": (C.c_int, [I32, I32, C.c_char_p, I32, I32, I32, I64, P, P, P, P, P, P,
                                                   P, I32, C.POINTER(P)]),
             "cpd_problem_dist_info": (C.c_int, [P, P]),
+            "cpd_problem_scale": (C.c_int, [P, I32, I32]),
+            "cpd_problem_get_scaling": (C.c_int, [P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -247,6 +250,16 @@ class Problem:
         self.nnz = int(lp.ATp[-1])
         self.mem = HOST
         return self
+
+    def scale(self, ruiz_iters=10, pock_chambolle=1):
+        """cpd_problem_scale: diagonal preconditioning (call before creating solvers)."""
+        _check(lib().cpd_problem_scale(self.h, int(ruiz_iters), int(pock_chambolle)))
+        return self
+
+    def scaling(self):
+        r, s = np.zeros(self.m), np.zeros(self.n)
+        _check(lib().cpd_problem_get_scaling(self.h, r.ctypes.data, s.ctypes.data))
+        return r, s
 
     def dist_info(self):
         out = (C.c_int64 * 10)()

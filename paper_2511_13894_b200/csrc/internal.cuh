@@ -133,6 +133,23 @@ struct cpd_problem {
     int64_t L = 0;                   // slice length of the split side
     std::vector<int64_t> rank_gofs[2], rank_len[2];   // every rank's owned part (global)
     void* comm = nullptr;            // ncclComm_t (split >= 0)
+    // ---- diagonal preconditioning (cpd_problem_scale; R-3): the device LP is
+    // the scaled one (A^ = diag(r) A diag(s), b^ = r b, c^ = s c, l^ = l/s, u^ = u/s);
+    // sr = r, ss = s, ir = 1/r, is = 1/s; lb0/ub0 the original bounds.  Unscaled: nulls.
+    bool scaled = false;
+    cpd::DBuf<double> sr, ss, ir, is, lb0, ub0;
+    bool uniform0 = false;
+    double l00 = 0.0, u00 = 0.0;
+    const double* w_m() const { return scaled ? ir.p : nullptr; }
+    const double* w_n() const { return scaled ? is.p : nullptr; }
+    const double* s_n() const { return scaled ? ss.p : nullptr; }
+    // original bounds of the owned n-side part
+    cpd::Bounds bounds_orig() const
+    {
+        if (!scaled) return bounds_own();
+        if (uniform0) return cpd::Bounds{nullptr, nullptr, l00, u00};
+        return cpd::Bounds{lb0.p, ub0.p, 0.0, 0.0};
+    }
     cpd::Bounds bounds() const
     {
         if (uniform_bounds) return cpd::Bounds{nullptr, nullptr, l0, u0};
@@ -202,6 +219,9 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
                  Gate g, double* red = nullptr);
 template <class Op>
 void launch_elem(Ctx& cx, int64_t N, const Op& op, Gate g, double* red = nullptr);
+
+// diagonal preconditioning of a problem (problem.cu)
+void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc);
 
 // distributed problem plumbing (dist.cu)
 void dist_destroy(cpd_problem* P);

@@ -218,13 +218,17 @@ __device__ __forceinline__ void score8(double rp2, double rd2, double pobj, doub
 
 // Dual-side terms of one column for z = c_j - (A^T y)_j (S-6 reading of P:109-131):
 // r_D_j = z - [l>-inf] max(z,0) + [u<inf] max(-z,0); bound part of the dual objective.
-__device__ __forceinline__ void dual_terms(double z, double lo, double hi, double& rd2, double& bnd)
+// w: 1 / s_j of a diagonally scaled problem (z = z^ / s_j in the original space, the
+// violation scales the same way; the bound terms l^ z^+ = l z+ need no weight)
+__device__ __forceinline__ void dual_terms(double z, double lo, double hi, double& rd2, double& bnd,
+                                           double w = 1.0)
 {
     double zp = z > 0.0 ? z : 0.0;
     double zm = -z > 0.0 ? -z : 0.0;
     double rd = z;
     if (lo > -INFINITY) { rd -= zp; bnd += lo * zp; }
     if (hi < INFINITY) { rd += zm; bnd -= hi * zm; }
+    rd *= w;
     rd2 += rd * rd;
 }
 
@@ -734,24 +738,18 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
     double acc[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-    // one warp per long row: lane-strided partials, xor-reduction (fixed order)
-    (void)s_w;
-    const int lane = threadIdx.x & 31;
-    const int nw = gridDim.x * (TPB / 32);
-    for (int l = (blockIdx.x * TPB + threadIdx.x) >> 5; l < P.nlong; l += nw) {
+    // one CTA per long row (heavy rows have tens of thousands of partials): strided
+    // per thread, then the block tree (fixed order)
+    for (int l = blockIdx.x; l < P.nlong; l += gridDim.x) {
         double sm[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) sm[v] = 0.0;
         const int64_t t0 = (int64_t)P.long_ptr[l] * P.pslot, t1 = (int64_t)P.long_ptr[l + 1] * P.pslot;
-#pragma unroll 4
-        for (int64_t t = t0 + lane; t < t1; t += 32)
+        for (int64_t t = t0 + threadIdx.x; t < t1; t += TPB)
 #pragma unroll
             for (int v = 0; v < NV; ++v) sm[v] += __ldcg(&P.lpart[t * 2 + v]);
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sm[v] += __shfl_xor_sync(0xffffffffu, sm[v], o);
-        if (lane == 0) {
+        block_sum<NV>(sm, s_w);
+        if (threadIdx.x == 0) {
             const int r = P.long_row[l];
             e.row(r, sm, vin, r, acc);
         }
@@ -1308,6 +1306,7 @@ struct EpiPrimalT {
     double* xn;
     const double* xac;
     double* xan;
+    const double* w = nullptr;   // 1/s (scaled problem): ||r_D|| in the original space
     __device__ void load(const Ctl* ctl)
     {
         tau = ctl->tau;
@@ -1339,7 +1338,7 @@ struct EpiPrimalT {
         // averages are read once per iteration: streamed (evict-first) so L2 keeps x+
         __stcs(&xan[j], xa + (xp - xa) * inv_t);   // (x+ - x_avg)/t as a multiply (<= 1 ulp)
         acc[0] += cj * x;
-        dual_terms(z, lo, hi, acc[1], acc[2]);
+        dual_terms(z, lo, hi, acc[1], acc[2], w ? w[j] : 1.0);
         acc[3] += isfinite(xp) ? 0.0 : 1.0;
     }
     // F(k): termination of iterate k (k >= 1, not a check iteration), P:124-126 / P:391-395.
@@ -1373,6 +1372,7 @@ struct EpiDual {
     const double* b;
     double *y, *ya, *ax;
     double sigma, inv_t;
+    const double* w = nullptr;   // 1/r (scaled problem): ||r_P|| in the original space
     __device__ void load(const Ctl* ctl)
     {
         sigma = ctl->sigma;
@@ -1393,7 +1393,7 @@ struct EpiDual {
         ax[i] = axn;
         const double yav = vin[3][li];
         __stcs(&ya[i], yav + (yp - yav) * inv_t);
-        const double r = bi - axn;
+        const double r = (bi - axn) * (w ? w[i] : 1.0);
         acc[0] += r * r;
         acc[1] += bi * yp;
         acc[2] += isfinite(yp) ? 0.0 : 1.0;
@@ -1427,6 +1427,8 @@ struct EpiCheckN {
     double eps_abs;
     const double *xc, *xac;
     int traj;
+    const double* w = nullptr;    // 1/s (scaled problem)
+    const double* sx = nullptr;   // s: the trajectory count tests x = s x^ against orig
     __device__ void load(const Ctl* ctl)
     {
         xc = X.at(ctl->k);
@@ -1440,16 +1442,20 @@ struct EpiCheckN {
         const double lo = bd.lo(j), hi = bd.hi(j);
         const double x = xc[j];
         const double xrj = xr[j];
+        const double wj = w ? w[j] : 1.0;
         acc[0] += cj * x;
-        dual_terms(cj - s[0], lo, hi, acc[1], acc[2]);
+        dual_terms(cj - s[0], lo, hi, acc[1], acc[2], wj);
         acc[3] += (x - xrj) * (x - xrj);
         if (two) {
             const double xa = xac[j];
             acc[4] += cj * xa;
-            dual_terms(cj - s[1], lo, hi, acc[5], acc[6]);
+            dual_terms(cj - s[1], lo, hi, acc[5], acc[6], wj);
             acc[7] += (xa - xrj) * (xa - xrj);
         }
-        if (traj) acc[8] += ((x - orig.lo(j) > eps_abs) && (orig.hi(j) - x > eps_abs)) ? 1.0 : 0.0;
+        if (traj) {
+            const double xo = sx ? x * sx[j] : x;
+            acc[8] += ((xo - orig.lo(j) > eps_abs) && (orig.hi(j) - xo > eps_abs)) ? 1.0 : 0.0;
+        }
     }
     __device__ void finalize(const double* tot, Ctl* ctl) const
     {
@@ -1465,12 +1471,13 @@ struct EpiCheckM {
     __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     const double *b, *y, *ya, *yr;
     double* axa;
+    const double* w = nullptr;   // 1/r (scaled problem)
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ void row(int i, const double* s, const double* const*, int, double* acc) const
     {
         axa[i] = s[0];
         const double bi = b[i];
-        const double r = bi - s[0];
+        const double r = (bi - s[0]) * (w ? w[i] : 1.0);
         acc[0] += r * r;
         const double yav = ya[i], yo = y[i], yri = yr[i];
         acc[1] += bi * yav;
@@ -1602,22 +1609,35 @@ struct OpBegin {
 
 // ||b||^2, ||c||^2 -> nb, nc, omega0, tau, sigma (S-8).
 struct OpNorms {
-    static constexpr int NS = 2;
+    static constexpr int NS = 4;
     const double *b, *c;
     int32_t n, m;
     double omega_in;   // > 0: given
+    // scaled problem (1/r, 1/s): the relative criteria use the ORIGINAL norms
+    // ||b|| = ||b^ / r||, ||c|| = ||c^ / s||; omega0 uses the scaled ones (cuPDLP)
+    const double* wm = nullptr;
+    const double* wn = nullptr;
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ void elem(int64_t i, double* acc) const
     {
-        if (i < m) acc[0] += b[i] * b[i];
-        if (i < n) acc[1] += c[i] * c[i];
+        if (i < m) {
+            acc[0] += b[i] * b[i];
+            const double bo = wm ? b[i] * wm[i] : b[i];
+            acc[2] += bo * bo;
+        }
+        if (i < n) {
+            acc[1] += c[i] * c[i];
+            const double co = wn ? c[i] * wn[i] : c[i];
+            acc[3] += co * co;
+        }
     }
     __device__ void finalize(const double* tot, Ctl* ctl) const
     {
-        ctl->nb = sqrt(tot[0]);
-        ctl->nc = sqrt(tot[1]);
+        const double nbs = sqrt(tot[0]), ncs = sqrt(tot[1]);
+        ctl->nb = sqrt(tot[2]);
+        ctl->nc = sqrt(tot[3]);
         if (omega_in > 0.0) ctl->omega = omega_in;
-        else ctl->omega = (ctl->nc > 1e-10 && ctl->nb > 1e-10) ? ctl->nc / ctl->nb : 1.0;
+        else ctl->omega = (ncs > 1e-10 && nbs > 1e-10) ? ncs / nbs : 1.0;
         ctl->tau = ctl->eta / ctl->omega;
         ctl->sigma = ctl->eta * ctl->omega;
         if (ctl->mode == MODE_PRIMAL_ONLY) ctl->target = ctl->eps_rel * (1.0 + ctl->nb);
@@ -1631,11 +1651,12 @@ struct EpiInitM {
     __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     const double *b, *y;
     double* ax;   // may be null (score only)
+    const double* w = nullptr;   // 1/r (scaled problem)
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ void row(int i, const double* s, const double* const*, int, double* acc) const
     {
         if (ax) ax[i] = s[0];
-        const double r = b[i] - s[0];
+        const double r = (b[i] - s[0]) * (w ? w[i] : 1.0);
         acc[0] += r * r;
         acc[1] += b[i] * y[i];
     }
@@ -1654,12 +1675,13 @@ struct EpiInitN {
     const double *c, *x;
     Bounds bd;
     int decide;   // 0: only store the score in ctl->last
+    const double* w = nullptr;   // 1/s (scaled problem)
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ void row(int j, const double* s, const double* const*, int, double* acc) const
     {
         const double cj = c[j];
         acc[0] += cj * x[j];
-        dual_terms(cj - s[0], bd.lo(j), bd.hi(j), acc[1], acc[2]);
+        dual_terms(cj - s[0], bd.lo(j), bd.hi(j), acc[1], acc[2], w ? w[j] : 1.0);
     }
     __device__ void finalize(const double* tot, Ctl* ctl) const
     {
@@ -1737,15 +1759,26 @@ struct EpiCorner {
     double eps_abs, obj_scale;
     uint64_t seed;
     int64_t jbase = 0;   // global index of local column 0 (distributed problems)
+    const double* w = nullptr;    // 1/s (scaled problem): the bound map tests z = z^ / s
+    const double* sx = nullptr;   // s: objective of the corner model in the scaled space
+    double* lho = nullptr;        // scaled problem: the model bounds in the original space
+    double* uho = nullptr;        //   (x* = s x^* where fixed, else the original bound)
+    Bounds ob{};
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ void row(int j, const double* s, const double* const*, int, double* acc) const
     {
         const double zj = c[j] - s[0];
         z[j] = zj;
+        const double zo = w ? zj * w[j] : zj;
         const double xj = x[j];
-        if (zj < -eps_abs) { lhat[j] = xj; acc[0] += 1.0; } else lhat[j] = bd.lo(j);
-        if (zj > eps_abs) { uhat[j] = xj; acc[1] += 1.0; } else uhat[j] = bd.hi(j);
-        chat[j] = obj ? obj[j] : obj_scale * u01(seed, jbase + j);
+        if (zo < -eps_abs) { lhat[j] = xj; acc[0] += 1.0; } else lhat[j] = bd.lo(j);
+        if (zo > eps_abs) { uhat[j] = xj; acc[1] += 1.0; } else uhat[j] = bd.hi(j);
+        if (lho) {
+            lho[j] = zo < -eps_abs ? xj * sx[j] : ob.lo(j);
+            uho[j] = zo > eps_abs ? xj * sx[j] : ob.hi(j);
+        }
+        const double oj = obj ? obj[j] : obj_scale * u01(seed, jbase + j);
+        chat[j] = sx ? oj * sx[j] : oj;
     }
     __device__ void finalize(const double* tot, Ctl* ctl) const
     {
@@ -1760,6 +1793,9 @@ struct OpStats {
     const double *x, *z, *lh, *uh;
     Bounds bd;
     double eps;
+    // scaled problem: x = s x^, z = z^ / s; bd and lh/uh are ORIGINAL-space bounds
+    const double* sx = nullptr;
+    const double* wz = nullptr;
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ static bool off(double x, double lo, double hi, double tol)
     {
@@ -1768,13 +1804,14 @@ struct OpStats {
     __device__ __forceinline__ void elem(int64_t jj, double* acc) const
     {
         const int j = (int)jj;
-        const double xj = x[j];
+        const double sj = sx ? sx[j] : 1.0;
+        const double xj = sx ? x[j] * sj : x[j];
         const bool o = off(xj, bd.lo(j), bd.hi(j), eps);
         acc[0] += o;
         acc[1] += off(xj, bd.lo(j), bd.hi(j), 0.0);
-        if (lh) acc[2] += off(xj, lh[j], uh[j], eps);
+        if (lh) acc[2] += off(xj, lh[j], uh[j], eps);   // lh/uh: model bounds in the original space
         if (z) {
-            const double az = fabs(z[j]);
+            const double az = fabs(wz ? z[j] * wz[j] : z[j]);
             acc[3] += az <= eps;
             acc[4] += o && az < eps;
         }

@@ -523,6 +523,106 @@ static void validate_csr(int32_t rows, int32_t cols, int64_t nnz, const Matrix& 
 
 }  // namespace cpd
 
+namespace cpd {
+// ------------------------------------------------------------ diagonal preconditioning
+// per row of a CSR layout: max |a| (mode 0) or sum |a| (mode 1); warp per row
+__global__ void k_row_absred(int32_t rows, const int32_t* p, const double* x, int mode, double* out)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double v = 0.0;
+        for (int64_t q = p[r] + lane; q < p[r + 1]; q += 32) {
+            const double a = fabs(x[q]);
+            v = mode ? v + a : (a > v ? a : v);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double t = __shfl_xor_sync(0xffffffffu, v, o);
+            v = mode ? v + t : (t > v ? t : v);
+        }
+        if (lane == 0) out[r] = v > 0.0 ? sqrt(v) : 1.0;
+    }
+}
+
+// x_q <- x_q / (rho_i kappa_j) for entry q of row `r`, column `c` of a layout:
+// A (swap 0): rho = rs[r], kappa = cs[c];  A^T (swap 1): rho = cs[c], kappa = rs[r]
+__global__ void k_apply_scale(int32_t rows, const int32_t* p, const int32_t* j, double* x, const double* rs,
+                              const double* cs, int swap)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5)
+        for (int64_t q = p[r] + lane; q < p[r + 1]; q += 32) {
+            const double den = swap ? cs[j[q]] * rs[r] : rs[r] * cs[j[q]];
+            x[q] = x[q] / den;
+        }
+}
+
+// op 0: v /= d; op 1: v *= d; op 2: out = 1 / v
+__global__ void k_vec_op(int64_t N, double* v, const double* d, int op, double* out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        if (op == 0) v[i] = v[i] / d[i];
+        else if (op == 1) v[i] = d[i] * v[i];
+        else out[i] = 1.0 / v[i];
+    }
+}
+
+// Ruiz (ruiz_iters passes of row / column max) then one Pock-Chambolle pass (row /
+// column sums, alpha = 1), exactly the oracle's orc_scale order of operations.
+void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc)
+{
+    const int32_t m = P->m, n = P->n;
+    const int sms = P->num_sms;
+    auto gw = [&](int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>((rows * 32 + 255) / 256, (int64_t)sms * 32)); };
+    P->sr.alloc(m);
+    P->ss.alloc(n);
+    P->ir.alloc(m);
+    P->is.alloc(n);
+    DBuf<double> rho(m), kap(n);
+    k_fill<<<grid_of(m, sms), 256>>>(m, P->sr.p, 1.0);
+    k_fill<<<grid_of(n, sms), 256>>>(n, P->ss.p, 1.0);
+    for (int pass = 0; pass < ruiz_iters + (pc ? 1 : 0); ++pass) {
+        const int mode = pass >= ruiz_iters ? 1 : 0;
+        k_row_absred<<<gw(m), 256>>>(m, P->A.p.p, P->A.x.p, mode, rho.p);
+        k_row_absred<<<gw(n), 256>>>(n, P->AT.p.p, P->AT.x.p, mode, kap.p);
+        k_apply_scale<<<gw(m), 256>>>(m, P->A.p.p, P->A.j.p, P->A.x.p, rho.p, kap.p, 0);
+        k_apply_scale<<<gw(n), 256>>>(n, P->AT.p.p, P->AT.j.p, P->AT.x.p, kap.p, rho.p, 1);
+        k_vec_op<<<grid_of(m, sms), 256>>>(m, P->sr.p, rho.p, 0, nullptr);
+        k_vec_op<<<grid_of(n, sms), 256>>>(n, P->ss.p, kap.p, 0, nullptr);
+        CPD_CUDA(cudaGetLastError());
+    }
+    // original bounds kept; the LP vectors become the scaled ones
+    P->lb0.alloc(n);
+    P->ub0.alloc(n);
+    CPD_CUDA(cudaMemcpy(P->lb0.p, P->lb.p, sizeof(double) * n, cudaMemcpyDeviceToDevice));
+    CPD_CUDA(cudaMemcpy(P->ub0.p, P->ub.p, sizeof(double) * n, cudaMemcpyDeviceToDevice));
+    P->uniform0 = P->uniform_bounds;
+    P->l00 = P->l0;
+    P->u00 = P->u0;
+    k_vec_op<<<grid_of(m, sms), 256>>>(m, P->b.p, P->sr.p, 1, nullptr);
+    k_vec_op<<<grid_of(n, sms), 256>>>(n, P->c.p, P->ss.p, 1, nullptr);
+    k_vec_op<<<grid_of(n, sms), 256>>>(n, P->lb.p, P->ss.p, 0, nullptr);
+    k_vec_op<<<grid_of(n, sms), 256>>>(n, P->ub.p, P->ss.p, 0, nullptr);
+    k_vec_op<<<grid_of(m, sms), 256>>>(m, P->sr.p, nullptr, 2, P->ir.p);
+    k_vec_op<<<grid_of(n, sms), 256>>>(n, P->ss.p, nullptr, 2, P->is.p);
+    CPD_CUDA(cudaGetLastError());
+    P->uniform_bounds = false;
+    // derived copies of the values
+    if (P->AT.sell.on) build_sell(P->AT, P->nnz, 1.25);
+    if (P->A.sell.on) build_sell(P->A, P->nnz, 1.25);
+    for (Matrix* M : {&P->A, &P->AT})
+        if (M->plan.short_on) {
+            const int g = (int)std::min<int64_t>(((int64_t)M->rows + 255) / 256, 8192);
+            k_short_fill<<<g, 256>>>(M->rows, M->plan.nslab, WLONG, M->p.p, M->j.p, M->x.p, M->plan.short_ptr.p,
+                                     M->plan.short_col.p, M->plan.short_val.p);
+        }
+    CPD_CUDA(cudaGetLastError());
+    CPD_CUDA(cudaDeviceSynchronize());
+    P->scaled = true;
+}
+}  // namespace cpd
+
 using namespace cpd;
 
 // Implementation of cpd_problem_create (called from the ABI layer).

@@ -222,7 +222,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
             if (seg.size() < 3) launch_dense();
         }
         if (dp.nlong > 0) {
-            const int gf = std::max(1, std::min(cx.P->num_sms * 8, (dp.nlong + TPB / 32 - 1) / (TPB / 32)));
+            const int gf = std::max(1, std::min(cx.P->num_sms * 8, dp.nlong));
             Gate g2 = g;
             g2.active = nullptr;
             k_finish<NV, Epi><<<gf, TPB, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, prev, red);
@@ -251,7 +251,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
     CPD_CUDA(cudaGetLastError());
     ++cx.launches;
     if (dp.nlong > 0) {
-        const int gf = std::max(1, std::min(cx.P->num_sms * 8, (dp.nlong + TPB / 32 - 1) / (TPB / 32)));
+        const int gf = std::max(1, std::min(cx.P->num_sms * 8, dp.nlong));
         Gate g2 = g;
         g2.active = nullptr;
         k_finish<NV, Epi><<<gf, TPB, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, gr, red);
@@ -383,8 +383,10 @@ static void eval_score(Ctx& cx, const double* x, const double* y, const double* 
     h.K = 1;
     cx.push_ctl(h);
     EpiInitM em{P->b_own(), y, nullptr};
+    em.w = P->w_m();
     pass<1>(cx, 0, fixed(rp.view(cx, 1, x)), none(), em, always());
     EpiInitN en{c, x, bd, 0};
+    en.w = P->w_n();
     pass<1>(cx, 1, fixed(rp.view(cx, 0, y)), none(), en, always());
     cx.pull_ctl();
     for (int i = 0; i < 8; ++i) out[i] = cx.h_ctl->last[i];
@@ -400,13 +402,17 @@ static void eval_norms(Ctx& cx, const double* b, const double* c, double* nb, do
     h.eta = 1.0;
     cx.push_ctl(h);
     OpNorms on{b, c, P->own_len[1], P->own_len[0], 1.0};
+    on.wm = P->w_m();
+    on.wn = P->w_n();
     elem(cx, std::max(P->own_len[1], P->own_len[0]), on, always(), true);
     cx.pull_ctl();
     *nb = cx.h_ctl->nb;
     *nc = cx.h_ctl->nc;
 }
 
-static void eval_stats(Ctx& cx, const double* x, const double* z, const double* lh, const double* uh,
+// internal: x, z are the solver's (scaled-space) vectors and lh/uh original-space
+// model bounds; else every array is already in the original space
+static void eval_stats(Ctx& cx, bool internal, const double* x, const double* z, const double* lh, const double* uh,
                        double eps, int64_t floor_, int64_t fix_lb, int64_t fix_ub, cpd_stats* out)
 {
     AuxScope aux(cx);
@@ -414,7 +420,11 @@ static void eval_stats(Ctx& cx, const double* x, const double* z, const double* 
     Ctl h{};
     h.K = 1;
     cx.push_ctl(h);
-    OpStats os{x, z, lh, uh, P->bounds_own(), eps};
+    OpStats os{x, z, lh, uh, P->bounds_orig(), eps};
+    if (internal) {
+        os.sx = P->s_n();
+        os.wz = P->w_n();
+    }
     elem(cx, P->own_len[1], os, always(), true);
     cx.pull_ctl();
     const double* o = cx.h_ctl->out;
@@ -466,6 +476,14 @@ __global__ void k_copy(int64_t N, double* dst, const double* src)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
          i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = src[i];
+}
+
+// op 0: dst = src / d (into the scaled space); op 1: dst = src * d (back to the original)
+__global__ void k_scale_vec(int64_t N, double* dst, const double* src, const double* d, int op)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = op ? src[i] * d[i] : src[i] / d[i];
 }
 
 __global__ void k_zero(int64_t N, double* dst)
@@ -521,6 +539,7 @@ struct cpd_solver {
     Ctx cx;
     // state vectors: n-side (x-like) of length own_len[1], m-side (y-like) own_len[0]
     DBuf<double> X0, X1, Xa0, Xa1, Xr, Y, Ya, Yr, AX, AXa, Ystar, Z, lhat, uhat, chat, objd, SN, SM;
+    DBuf<double> LHo, UHo, TX, TY;   // scaled problems: original-space model bounds; unscale scratch
     // replicas of the split side (world * L): current vector / its average
     DBuf<double> RV, RA;
     DBuf<int64_t> trk, troff;
@@ -586,6 +605,8 @@ struct cpd_solver {
         for (auto e : ev1) cudaEventDestroy(e);
         if (h_active) cudaFreeHost(h_active);
     }
+    const double* lh_orig() const { return P->scaled ? LHo.p : lhat.p; }
+    const double* uh_orig() const { return P->scaled ? UHo.p : uhat.p; }
     int32_t nO() const { return P->own_len[1]; }
     int32_t mO() const { return P->own_len[0]; }
     double* Xp(int par) { return par ? X1.p : X0.p; }
@@ -630,12 +651,16 @@ struct cpd_solver {
         const double* c = obj_of(rc.kind);
         const Bounds bd = bounds_of(rc.kind);
         OpNorms on{P->b_own(), c, n, m, rc.omega_in};
+        on.wm = P->w_m();
+        on.wn = P->w_n();
         elem(cx, std::max(n, m), on, always(), true);
         OpBegin ob{rc.xs, rc.ys, bd, X0.p, Xa0.p, Xa1.p, Xr.p, Y.p, Ya.p, Yr.p, n, m, rc.ys ? 0 : 1};
         elem(cx, std::max(n, m), ob, always(), false);
         EpiInitM em{P->b_own(), Y.p, AX.p};
+        em.w = P->w_m();
         pass<1>(cx, 0, fixed(rp.view(cx, 1, X0.p)), none(), em, always());
         EpiInitN en{c, X0.p, bd, 1};
+        en.w = P->w_n();
         // the batch's K1 gathers the y replica: refresh it here (split m-side)
         refresh(cx, 0, fixed(Y.p), RV.p, always());
         pass<1>(cx, 1, gsrc(0, fixed(Y.p), RV.p), none(), en, always());
@@ -655,7 +680,7 @@ struct cpd_solver {
         const int K = prm.check_every;
         const double* c = obj_of(kind);
         const Bounds bd = bounds_of(kind);
-        const Bounds orig = P->bounds_own();
+        const Bounds orig = P->bounds_orig();
         const PingPong X{{X0.p, X1.p}}, Xa{{Xa0.p, Xa1.p}};
         auto rec = [&](std::vector<cudaEvent_t>& ev, int node) {
             if (!prm.profile) return;
@@ -666,6 +691,8 @@ struct cpd_solver {
         // restart check: A^T pass (current y and average y) + A pass (A x_avg) + decision
         {
             EpiCheckN e{c, bd, orig, X, Xa, Xr.p, prm.restart ? 1 : 0, 0.0, nullptr, nullptr, 0};
+            e.w = P->w_n();
+            e.sx = P->s_n();
             Gate g{GATE_CHECK, 0, NODE_CHECK_N, active.p};
             rec(ev0, NODE_CHECK_N);
             // RV holds y_k (refreshed after every dual step); RA <- average of y
@@ -677,6 +704,7 @@ struct cpd_solver {
             }
             rec(ev1, NODE_CHECK_N);
             EpiCheckM em{P->b_own(), Y.p, Ya.p, Yr.p, AXa.p};
+            em.w = P->w_m();
             Gate gm{GATE_CHECK, 0, NODE_CHECK_M, active.p};
             rec(ev0, NODE_CHECK_M);
             refresh(cx, 1, VecSel{Xa0.p, Xa1.p, 2}, RA.p, gm);
@@ -696,9 +724,11 @@ struct cpd_solver {
             const VecSel ysrc = gsrc(0, fixed(Y.p), RV.p);
             if (kind == 0 && P->uniform_bounds) {   // scalar bounds: 3 staged per-row inputs
                 EpiPrimalT<false> e1{c, bd, X, Xa, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+                e1.w = P->w_n();
                 pass<1>(cx, 1, ysrc, none(), e1, g1);
             } else {
                 EpiPrimalT<true> e1{c, bd, X, Xa, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+                e1.w = P->w_n();
                 pass<1>(cx, 1, ysrc, none(), e1, g1);
             }
             // x_{k+1} replica for the dual step's gathers (split n-side); the
@@ -706,6 +736,7 @@ struct cpd_solver {
             refresh(cx, 1, VecSel{X0.p, X1.p, 1}, RV.p, g2);
             rec(ev1, n1);
             EpiDual e2{P->b_own(), Y.p, Ya.p, AX.p, 0.0, 0.0};
+            e2.w = P->w_m();
             rec(ev0, n2);
             pass<1>(cx, 0, gsrc(1, VecSel{X0.p, X1.p, 1}, RV.p), none(), e2, g2);
             // y_{k+1} replica for the next primal step (split m-side); k already advanced
@@ -892,6 +923,17 @@ struct cpd_solver {
             cx.push_ctl(h);
             EpiCorner ec{P->c_own(), Xp(cur_par), P->bounds_own(), Z.p, lhat.p, uhat.p, chat.p, obj, cp.eps_abs,
                          cp.obj_scale, cp.seed, P->gofs[1]};
+            if (P->scaled) {   // bound map on z = z^/s; objective s * obj; model bounds also in the original space
+                if (!LHo.p) {
+                    LHo.alloc(n);
+                    UHo.alloc(n);
+                }
+                ec.w = P->w_n();
+                ec.sx = P->s_n();
+                ec.lho = LHo.p;
+                ec.uho = UHo.p;
+                ec.ob = P->bounds_orig();
+            }
             pass<1>(cx, 1, fixed(rp.view(cx, 0, Ystar.p)), none(), ec, always());
             cx.pull_ctl();
             fix_lb = (int64_t)cx.h_ctl->out[0];
@@ -899,8 +941,8 @@ struct cpd_solver {
         }
         have_corner = true;
         if (before)
-            eval_stats(cx, Xp(cur_par), Z.p, lhat.p, uhat.p, cp.eps_abs, cp.candidate_floor, fix_lb, fix_ub,
-                       before);
+            eval_stats(cx, true, Xp(cur_par), Z.p, lh_orig(), uh_orig(), cp.eps_abs, cp.candidate_floor, fix_lb,
+                       fix_ub, before);
         if (!eta_known) {
             // no phase 1 on this solver: step size as phase 1 would have chosen it
             if (prm.step_size > 0.0) eta_phase1 = prm.step_size;
@@ -929,8 +971,8 @@ struct cpd_solver {
         CPD_CUDA(cudaGetLastError());
         ++cx.launches;
         if (after)
-            eval_stats(cx, Xp(cur_par), Z.p, lhat.p, uhat.p, cp.eps_abs, cp.candidate_floor, fix_lb, fix_ub,
-                       after);
+            eval_stats(cx, true, Xp(cur_par), Z.p, lh_orig(), uh_orig(), cp.eps_abs, cp.candidate_floor, fix_lb,
+                       fix_ub, after);
     }
 
     // x: n-side vector, y: m-side vector, both GLOBAL length; each rank takes its part.
@@ -945,11 +987,24 @@ struct cpd_solver {
             if (y) CPD_CUDA(cudaMemcpyAsync(Y.p, y + P->gofs[0], sizeof(double) * mO(), kind, cx.st));
             else CPD_CUDA(cudaMemsetAsync(Y.p, 0, sizeof(double) * mO(), cx.st));
         }
+        if (P->scaled) {   // original-space input: x^ = x / s, y^ = y / r
+            scale_vec(nO(), X0.p, X0.p, P->ss.p, 0);
+            scale_vec(mO(), Y.p, Y.p, P->sr.p, 0);
+        }
         cx.sync();
         cur_par = 0;
         run_active = false;
         have_corner = false;
         eta_known = false;
+    }
+
+    void scale_vec(int64_t N, double* dst, const double* src, const double* d, int op)
+    {
+        if (N <= 0) return;
+        const int g = (int)std::min<int64_t>(cx.grid_elem, (N + 255) / 256);
+        k_scale_vec<<<g, 256, 0, cx.st>>>(N, dst, src, d, op);
+        CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
     }
 
     void compute_z()
@@ -986,12 +1041,25 @@ struct cpd_solver {
         cx.sync();
     }
 
+    // Original-space iterate: x = s x^, y = r y^, z = z^ / s (scaled problems).
     void get_iterate(double* x, double* y, double* z, int mem)
     {
         if (z) compute_z();
-        if (x) gather_full(1, Xp(cur_par), x, mem);
-        if (y) gather_full(0, Y.p, y, mem);
-        if (z) gather_full(1, Z.p, z, mem);
+        const double *xs = Xp(cur_par), *ys = Y.p, *zs = Z.p;
+        if (P->scaled) {
+            if (!TX.p) {
+                TX.alloc(std::max(nO(), 1));
+                TY.alloc(std::max(mO(), 1));
+            }
+            if (x) scale_vec(nO(), TX.p, xs, P->ss.p, 1), xs = TX.p, gather_full(1, xs, x, mem);
+            if (y) scale_vec(mO(), TY.p, ys, P->sr.p, 1), ys = TY.p, gather_full(0, ys, y, mem);
+            if (z) scale_vec(nO(), TX.p, zs, P->is.p, 1), zs = TX.p, gather_full(1, zs, z, mem);
+            cx.sync();
+            return;
+        }
+        if (x) gather_full(1, xs, x, mem);
+        if (y) gather_full(0, ys, y, mem);
+        if (z) gather_full(1, zs, z, mem);
         cx.sync();
     }
 
@@ -1053,6 +1121,28 @@ int cpd_problem_create_dist(int32_t rank, int32_t world, const char id[128], int
     if (!out) return fail(CPD_E_ARG, "out is NULL");
     *out = cpd_problem_create_dist_impl(rank, world, id, partition, m, n, nnz, AT_rowptr, AT_col, AT_val, b, c,
                                         lb, ub, device);
+    ABI_END
+}
+
+int cpd_problem_scale(cpd_problem* p, int32_t ruiz_iters, int32_t pock_chambolle)
+{
+    ABI_BEGIN
+    if (!p || ruiz_iters < 0 || ruiz_iters > 1000) return fail(CPD_E_ARG, "bad argument");
+    if (p->split >= 0) return fail(CPD_E_ARG, "scaling of distributed problems is not supported");
+    if (p->scaled) return fail(CPD_E_STATE, "problem is already scaled");
+    CPD_CUDA(cudaSetDevice(p->device));
+    cpd::scale_problem(p, ruiz_iters, pock_chambolle ? 1 : 0);
+    ABI_END
+}
+
+int cpd_problem_get_scaling(const cpd_problem* p, double* r, double* s)
+{
+    ABI_BEGIN
+    if (!p) return fail(CPD_E_ARG, "NULL problem");
+    if (!p->scaled) return fail(CPD_E_STATE, "problem is not scaled");
+    CPD_CUDA(cudaSetDevice(p->device));
+    if (r) CPD_CUDA(cudaMemcpy(r, p->sr.p, sizeof(double) * p->m, cudaMemcpyDeviceToHost));
+    if (s) CPD_CUDA(cudaMemcpy(s, p->ss.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
     ABI_END
 }
 
@@ -1233,8 +1323,8 @@ int cpd_get_stats(const cpd_solver* cs, int64_t candidate_floor, cpd_stats* out)
     auto* s = const_cast<cpd_solver*>(cs);
     CPD_CUDA(cudaSetDevice(s->P->device));
     s->compute_z();
-    eval_stats(s->cx, s->Xp(s->cur_par), s->Z.p, s->have_corner ? s->lhat.p : nullptr,
-               s->have_corner ? s->uhat.p : nullptr, s->have_corner ? s->corner_eps : s->prm.eps_abs,
+    eval_stats(s->cx, true, s->Xp(s->cur_par), s->Z.p, s->have_corner ? s->lh_orig() : nullptr,
+               s->have_corner ? s->uh_orig() : nullptr, s->have_corner ? s->corner_eps : s->prm.eps_abs,
                candidate_floor, s->have_corner ? s->fix_lb : 0, s->have_corner ? s->fix_ub : 0, out);
     ABI_END
 }
@@ -1280,6 +1370,12 @@ int cpd_problem_score(const cpd_problem* p, const double* x, const double* y, in
     const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (nO) CPD_CUDA(cudaMemcpy(dx.p, x + p->gofs[1], sizeof(double) * nO, kind));
     if (mO) CPD_CUDA(cudaMemcpy(dy.p, y + p->gofs[0], sizeof(double) * mO, kind));
+    if (p->scaled) {   // original-space point -> scaled
+        if (nO) k_scale_vec<<<(int)std::min<int64_t>(4096, (nO + 255) / 256), 256, 0, cx.st>>>(nO, dx.p, dx.p, p->ss.p, 0);
+        if (mO) k_scale_vec<<<(int)std::min<int64_t>(4096, (mO + 255) / 256), 256, 0, cx.st>>>(mO, dy.p, dy.p, p->sr.p, 0);
+        CPD_CUDA(cudaGetLastError());
+        cx.sync();
+    }
     double nb, nc;
     eval_norms(cx, p->b_own(), p->c_own(), &nb, &nc);
     eval_score(cx, dx.p, dy.p, p->c_own(), p->bounds_own(), nb, nc, out);
@@ -1306,7 +1402,7 @@ int cpd_compute_stats(const cpd_problem* p, const double* x, const double* z, co
             if (nO) CPD_CUDA(cudaMemcpy(b[i].p, src[i] + p->gofs[1], sizeof(double) * nO, kind));
             dev[i] = b[i].p;
         }
-    eval_stats(cx, dev[0], dev[1], dev[2], dev[3], eps_abs, candidate_floor, 0, 0, out);
+    eval_stats(cx, false, dev[0], dev[1], dev[2], dev[3], eps_abs, candidate_floor, 0, 0, out);
     ABI_END
 }
 
