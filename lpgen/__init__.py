@@ -50,6 +50,7 @@ class LP:
     y0: Optional[np.ndarray] = None
     z0: Optional[np.ndarray] = None
     opt: Optional[float] = None
+    sense: Optional[np.ndarray] = None   # int8 [m]: 0 '=', 1 '<=', 2 '>=' (None: all '=')
     name: str = ""
     meta: dict = dataclasses.field(default_factory=dict)
 
@@ -258,7 +259,7 @@ def gen_transport(S=2000, T=2000, seed=3, amount_max=1000, cost_max=100, name="c
               meta=dict(recipe="transport", seed=seed, S=S, T=T, total=int(s.sum())))
 
 
-def gen_multicommodity(G=100, K=50, seed=4, name="c4"):
+def gen_multicommodity(G=100, K=50, seed=4, name="c4", implicit=False):
     """BASELINE.json config 4: grid multicommodity flow.
 
     Arcs both directions between 4-neighbours of a GxG grid; cost ~U[1,10],
@@ -268,6 +269,10 @@ def gen_multicommodity(G=100, K=50, seed=4, name="c4"):
     K*V + a (sum_k x_ka + s_a = cap_a). Feasible by construction: each commodity
     routed on its row-then-column L-path; a capacity below the routed load is
     raised to load+1 (count recorded in meta).
+
+    implicit=True: the capacity rows are inequalities sum_k x_ka <= cap_a (row
+    sense 1) without slack columns, the form practical LP solvers use and the
+    paper's corner rule for.
     """
     rng = np.random.default_rng(seed)
     V = G * G
@@ -349,10 +354,16 @@ def gen_multicommodity(G=100, K=50, seed=4, name="c4"):
         b[k * V + dst[k]] -= dem[k]
     b[K * V:] = cap
     c = np.concatenate([np.tile(cost, K), np.zeros(NA)])
+    meta = dict(recipe="multicommodity", seed=seed, G=G, K=K, NA=NA, raised_caps=int(raised.sum()),
+                implicit=implicit)
+    if implicit:   # drop the slack columns; capacity rows become '<='
+        nf = K * NA
+        lp = LP(m=m, n=nf, ATp=ATp[:nf + 1].copy(), ATj=ATj[:3 * nf].copy(), ATx=ATx[:3 * nf].copy(), b=b,
+                c=c[:nf].copy(), lb=np.zeros(nf), ub=np.full(nf, np.inf), x0=x0[:nf].copy(), name=name, meta=meta)
+        lp.sense = np.concatenate([np.zeros(K * V, np.int8), np.ones(NA, np.int8)])
+        return lp
     return LP(m=m, n=n, ATp=ATp, ATj=ATj, ATx=ATx, b=b, c=c, lb=np.zeros(n),
-              ub=np.full(n, np.inf), x0=x0, name=name,
-              meta=dict(recipe="multicommodity", seed=seed, G=G, K=K, NA=NA,
-                        raised_caps=int(raised.sum())))
+              ub=np.full(n, np.inf), x0=x0, name=name, meta=meta)
 
 
 # name -> (factory, kwargs). "full" sizes are BASELINE.json's; "-s" variants are the
@@ -368,6 +379,8 @@ CONFIGS = {
     "c2-s": (gen_sparse, dict(m=1000, n=5000, per_col=8, seed=12, ub=100.0, name="c2-s")),
     "c3-s": (gen_transport, dict(S=60, T=50, seed=13, name="c3-s")),
     "c4-s": (gen_multicommodity, dict(G=10, K=5, seed=14, name="c4-s")),
+    "c4-ineq": (gen_multicommodity, dict(G=100, K=50, seed=4, name="c4-ineq", implicit=True)),
+    "c4-s-ineq": (gen_multicommodity, dict(G=10, K=5, seed=14, name="c4-s-ineq", implicit=True)),
     "c5-s": (gen_sparse, dict(m=20_000, n=100_000, per_col=12, seed=15, ub=100.0,
                               zipf=1.2, name="c5-s")),
 }

@@ -41,7 +41,7 @@ class LPStruct(C.Structure):
     _fields_ = [("m", C.c_int32), ("n", C.c_int32),
                 ("Ap", C.c_void_p), ("Aj", C.c_void_p), ("Ax", C.c_void_p),
                 ("ATp", C.c_void_p), ("ATj", C.c_void_p), ("ATx", C.c_void_p),
-                ("b", C.c_void_p)]
+                ("b", C.c_void_p), ("sense", C.c_void_p)]
 
 
 class Params(C.Structure):
@@ -116,6 +116,8 @@ def lib():
             L.orc_stats.argtypes = [C.c_int32, C.c_int32, P, P, P, P, P, P, C.c_double,
                                     C.c_int64, C.POINTER(Stats)]
             L.orc_scale.argtypes = [C.c_int32, C.c_int32, P, P, P, C.c_int32, C.c_int32, P, P]
+            L.orc_corner_senses.restype = C.c_int64
+            L.orc_corner_senses.argtypes = [C.c_int32, P, P, C.c_double, P]
             L.orc_set_original.argtypes = [P, C.POINTER(LPStruct), P, P, P, P, P]
             _lib = L
     return _lib
@@ -159,9 +161,20 @@ class OracleLP:
         self.c = _f64(lp.c)
         self.lb = _f64(lp.lb)
         self.ub = _f64(lp.ub)
+        sense = getattr(lp, "sense", None)
+        self.sense = None if sense is None else np.ascontiguousarray(sense, dtype=np.int8)
         self.s = LPStruct(self.m, self.n, _p(self.Ap), _p(self.Aj), _p(self.Ax),
-                          _p(self.ATp), _p(self.ATj), _p(self.ATx), _p(self.b))
+                          _p(self.ATp), _p(self.ATj), _p(self.ATx), _p(self.b), _p(self.sense))
         self.nb = float(L.orc_norm2(self.m, _p(self.b)))
+
+    def with_senses(self, sense):
+        """The same LP with other row senses (shares every array)."""
+        import copy
+        o = copy.copy(self)
+        o.sense = None if sense is None else np.ascontiguousarray(sense, dtype=np.int8)
+        o.s = LPStruct(self.m, self.n, _p(self.Ap), _p(self.Aj), _p(self.Ax),
+                       _p(self.ATp), _p(self.ATj), _p(self.ATx), _p(self.b), _p(o.sense))
+        return o
 
     def A_times(self, v):
         out = np.zeros(self.m)
@@ -271,7 +284,7 @@ class ScaledLP:
         tx = np.zeros(max(nnz, 1))
         lib().orc_transpose(m, n, _p(olp.Ap), _p(olp.Aj), _p(Ax), _p(tp), _p(tj), _p(tx))
         ns = types.SimpleNamespace(m=m, n=n, ATp=tp, ATj=tj[:nnz], ATx=tx[:nnz], b=self.r * olp.b,
-                                   c=self.s * olp.c, lb=olp.lb / self.s, ub=olp.ub / self.s)
+                                   c=self.s * olp.c, lb=olp.lb / self.s, ub=olp.ub / self.s, sense=olp.sense)
         self.olp = OracleLP(ns)
         self.orig = olp
 
@@ -306,9 +319,12 @@ def corner_push_scaled(olp: OracleLP, sl: "ScaledLP", x, y, params: Params = Non
     p2.max_iters = max_iters
     p2.primal_weight = 0.0
     target = params.eps_rel * (1.0 + olp.nb)
-    r = Run(sl.olp, p2, c=sl.s * ch, lb=lh / sl.s, ub=uh / sl.s, x_init=_f64(x) / sl.s, y_init=None,
+    shat, nrows_eq = corner_senses(olp, y, eps_abs)
+    sc_m = sl.olp.with_senses(shat) if olp.sense is not None else sl.olp
+    or_m = olp.with_senses(shat) if olp.sense is not None else olp
+    r = Run(sc_m, p2, c=sl.s * ch, lb=lh / sl.s, ub=uh / sl.s, x_init=_f64(x) / sl.s, y_init=None,
             mode=MODE_PRIMAL_ONLY, target=target, min_iters=min_iters, eta=eta)
-    r.set_original(olp, ch, lh, uh, sl.r, sl.s)
+    r.set_original(or_m, ch, lh, uh, sl.r, sl.s)
     r.run(np.iinfo(np.int64).max)
     xh, _ = r.get()
     xh = sl.s * xh
@@ -316,7 +332,18 @@ def corner_push_scaled(olp: OracleLP, sl: "ScaledLP", x, y, params: Params = Non
     after = stats(olp.m, xh, z, olp.lb, olp.ub, lh, uh, eps_abs, floor)
     before["fix_lb"] = after["fix_lb"] = fl
     before["fix_ub"] = after["fix_ub"] = fu
-    return xh, y, z, res, before, after, dict(lhat=lh, uhat=uh, chat=ch, target=target)
+    return xh, y, z, res, before, after, dict(lhat=lh, uhat=uh, chat=ch, target=target, shat=shat,
+                                              rows_eq=nrows_eq)
+
+
+def corner_senses(olp: OracleLP, y, eps_abs=1e-6):
+    """Corner-model row senses: (shat, #rows made equality)."""
+    if olp.sense is None:
+        return None, 0
+    shat = np.zeros(olp.m, np.int8)
+    y = _f64(y)
+    k = lib().orc_corner_senses(olp.m, _p(olp.sense), _p(y), eps_abs, _p(shat))
+    return shat, int(k)
 
 
 def solve(olp: OracleLP, params: Params = None, **kw):
@@ -371,12 +398,14 @@ def corner_push(olp: OracleLP, x, y, params: Params = None, eps_abs=1e-6, obj_sc
     lh, uh, ch, fl, fu = corner_model(olp, x, z, eps_abs, obj_scale, seed)
     if obj is not None:
         ch = _f64(obj)
+    shat, nrows_eq = corner_senses(olp, y, eps_abs)
     before = stats(olp.m, x, z, olp.lb, olp.ub, lh, uh, eps_abs, floor)
     p2 = default_params(**{k: getattr(params, k) for k, _ in Params._fields_})
     p2.max_iters = max_iters
     p2.primal_weight = 0.0   # fresh omega from ||chat||/||b|| (S-8)
     target = params.eps_rel * (1.0 + olp.nb)
-    r = Run(olp, p2, c=ch, lb=lh, ub=uh, x_init=x, y_init=None, mode=MODE_PRIMAL_ONLY,
+    mhat = olp.with_senses(shat) if olp.sense is not None else olp
+    r = Run(mhat, p2, c=ch, lb=lh, ub=uh, x_init=x, y_init=None, mode=MODE_PRIMAL_ONLY,
             target=target, min_iters=min_iters, eta=eta)
     r.run(np.iinfo(np.int64).max)
     xh, _ = r.get()
@@ -384,4 +413,5 @@ def corner_push(olp: OracleLP, x, y, params: Params = None, eps_abs=1e-6, obj_sc
     after = stats(olp.m, xh, z, olp.lb, olp.ub, lh, uh, eps_abs, floor)
     before["fix_lb"] = after["fix_lb"] = fl
     before["fix_ub"] = after["fix_ub"] = fu
-    return xh, y, z, res, before, after, dict(lhat=lh, uhat=uh, chat=ch, target=target)
+    return xh, y, z, res, before, after, dict(lhat=lh, uhat=uh, chat=ch, target=target, shat=shat,
+                                              rows_eq=nrows_eq)

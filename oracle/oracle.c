@@ -39,6 +39,8 @@ typedef struct {
     const int32_t *Ap, *Aj; const double *Ax;     /* CSR(A)   (m rows) */
     const int32_t *ATp, *ATj; const double *ATx;  /* CSR(A^T) (n rows) */
     const double *b;                              /* m */
+    const int8_t *sense;   /* m or NULL (all '='): 0 '=' , 1 '<=' (Ax <= b), 2 '>=' (Ax >= b)
+                              (inequality rows handled implicitly) */
 } orc_lp;
 
 typedef struct {
@@ -144,6 +146,26 @@ static double now_s(void)
 
 /* ------------------------------------------------------- residuals, score */
 
+/* Row i of r_P = b - A x counts its violation only:
+ * '=' r;  '<=' (Ax <= b, feasible when r >= 0) min(r, 0);  '>=' max(r, 0). */
+static double row_violation(const orc_lp *lp, int32_t i, double r)
+{
+    int s = lp->sense ? lp->sense[i] : 0;
+    if (s == 1) return r < 0.0 ? r : 0.0;
+    if (s == 2) return r > 0.0 ? r : 0.0;
+    return r;
+}
+
+/* Dual sign constraint of row i for L = c^T x + y^T (b - A x): '>=' rows y >= 0,
+ * '<=' rows y <= 0, '=' free (projection of the dual step). */
+static double dual_proj(const orc_lp *lp, int32_t i, double v)
+{
+    int s = lp->sense ? lp->sense[i] : 0;
+    if (s == 1) return v < 0.0 ? v : 0.0;
+    if (s == 2) return v > 0.0 ? v : 0.0;
+    return v;
+}
+
 /* KKT score of (x, y) for objective c and bounds [l, u] (S-3, S-6):
  *   z = c - A^T y;  r_P = b - A x
  *   r_D_j = z_j - [l_j > -inf] max(z_j,0) + [u_j < inf] max(-z_j,0)  (violation part)
@@ -159,7 +181,7 @@ void orc_score(const orc_lp *lp, const double *c, const double *l, const double 
     orc_spmv(n, lp->ATp, lp->ATj, lp->ATx, y, aty);
     double rp2 = 0.0;
     for (int32_t i = 0; i < m; ++i) {
-        double r = lp->b[i] - ax[i];
+        double r = row_violation(lp, i, lp->b[i] - ax[i]);
         rp2 += r * r;
     }
     double rd2 = 0.0, pobj = 0.0, bound_terms = 0.0;
@@ -377,7 +399,7 @@ static double primal_res(orc_state *s, const double *x)
     orc_spmv(lp->m, lp->Ap, lp->Aj, lp->Ax, x, s->axbar);
     double r2 = 0.0;
     for (int32_t i = 0; i < lp->m; ++i) {
-        double r = lp->b[i] - s->axbar[i];
+        double r = row_violation(lp, i, lp->b[i] - s->axbar[i]);
         r2 += r * r;
     }
     return sqrt(r2);
@@ -400,7 +422,8 @@ int orc_run(orc_state *s, int64_t steps)
         /* y+ = y + sigma (b - A (2 x+ - x)) */
         for (int32_t j = 0; j < n; ++j) s->xbar[j] = 2.0 * s->xn[j] - s->x[j];
         orc_spmv(m, lp->Ap, lp->Aj, lp->Ax, s->xbar, s->axbar);
-        for (int32_t i = 0; i < m; ++i) s->yn[i] = s->y[i] + sigma * (lp->b[i] - s->axbar[i]);
+        for (int32_t i = 0; i < m; ++i)
+            s->yn[i] = dual_proj(lp, i, s->y[i] + sigma * (lp->b[i] - s->axbar[i]));
         int bad = 0;
         for (int32_t j = 0; j < n; ++j) bad |= !isfinite(s->xn[j]);
         for (int32_t i = 0; i < m; ++i) bad |= !isfinite(s->yn[i]);
@@ -513,6 +536,20 @@ void orc_corner_model(int32_t n, const double *x, const double *z, const double 
     }
     *fix_lb = fl;
     *fix_ub = fu;
+}
+
+/* Corner model row senses: an inequality row whose slack has a
+ * non-trivial reduced cost (|y_i| > eps_abs) becomes an equality ("fixing the slack
+ * upper bound to zero"); returns the number of rows changed. */
+int64_t orc_corner_senses(int32_t m, const int8_t *sense, const double *y, double eps_abs, int8_t *shat)
+{
+    int64_t k = 0;
+    for (int32_t i = 0; i < m; ++i) {
+        int s = sense ? sense[i] : 0;
+        if (s != 0 && fabs(y[i]) > eps_abs) { shat[i] = 0; k++; }
+        else shat[i] = (int8_t)s;
+    }
+    return k;
 }
 
 /* Off-bound test (Fig. 1 axis P:336; S-10): strictly inside by > tol

@@ -66,6 +66,7 @@ struct Plan {
     DBuf<int32_t> long_row, long_ptr, long_ents;
     int32_t nent = 0, nlong = 0;
     int32_t warp = 0;     // 1: warp-item plan for k_csrw (<= 32 rows / <= WCAP nnz per item)
+    int32_t nfin_heavy = 0;   // long rows finished by a CTA each (long_ents = finish order)
     std::vector<int32_t> seg;   // item ranges launched separately: rows items, then one per column slab
     int32_t nheavy = 0, nhb = 0;          // heavy rows (k_dense) and column blocks of HB
     DBuf<PlanEntry> dense_ent;            // {slot, block, q0, q1} grouped by block

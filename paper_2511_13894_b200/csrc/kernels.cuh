@@ -43,6 +43,7 @@ constexpr int HEAVY_MIN = 65536; // k_dense: rows with at least this many nonzer
 constexpr int HB = 8192;         // k_dense: columns per dense block (64 KB of the vector in smem)
 constexpr int DCHUNK = 512;      // k_dense: entries per item (balances the Zipf head across warps)
 constexpr int TPB_D = 512;
+constexpr int FIN_SPLIT = 1024;  // k_finish: rows with more partials get a CTA, the rest a warp
 
 enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2 };
 enum { ST_RUNNING = -1, ST_CONVERGED = 0, ST_ITER_LIMIT = 1, ST_TIME_LIMIT = 2, ST_FAIL = 3 };
@@ -69,7 +70,8 @@ struct DevPlan {
     double* short_part;           // [NV][rows] running sums across slab passes
     const int32_t* long_row;   // [nlong] row index of each long row
     const int32_t* long_ptr;   // [nlong + 1] piece slots of each long row (column order)
-    const int32_t* long_ents;  // unused (kept for layout stability)
+    const int32_t* long_ents;  // k_finish order: nfin_heavy rows (a CTA each), then the rest (a warp each)
+    int32_t nfin_heavy;
     double* lpart;             // [pieces * GW * 2] warp partial sums (NV <= 2)
 };
 
@@ -738,9 +740,11 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
     double acc[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-    // one CTA per long row (heavy rows have tens of thousands of partials): strided
-    // per thread, then the block tree (fixed order)
-    for (int l = blockIdx.x; l < P.nlong; l += gridDim.x) {
+    // rows with many partials (heavy rows: tens of thousands): one CTA each, strided
+    // per thread then the block tree; the others one warp each, lane-strided then the
+    // xor tree (fixed order either way)
+    for (int h = blockIdx.x; h < P.nfin_heavy; h += gridDim.x) {
+        const int l = P.long_ents[h];
         double sm[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) sm[v] = 0.0;
@@ -752,6 +756,28 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
         if (threadIdx.x == 0) {
             const int r = P.long_row[l];
             e.row(r, sm, vin, r, acc);
+        }
+    }
+    {
+        const int lane = threadIdx.x & 31;
+        const int nw = gridDim.x * (TPB / 32);
+        for (int h = P.nfin_heavy + ((blockIdx.x * TPB + threadIdx.x) >> 5); h < P.nlong; h += nw) {
+            const int l = P.long_ents[h];
+            double sm[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) sm[v] = 0.0;
+            const int64_t t0 = (int64_t)P.long_ptr[l] * P.pslot, t1 = (int64_t)P.long_ptr[l + 1] * P.pslot;
+            for (int64_t t = t0 + lane; t < t1; t += 32)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) sm[v] += __ldcg(&P.lpart[t * 2 + v]);
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sm[v] += __shfl_xor_sync(0xffffffffu, sm[v], o);
+            if (lane == 0) {
+                const int r = P.long_row[l];
+                e.row(r, sm, vin, r, acc);
+            }
         }
     }
     grid_finalize<NS>(acc, bpart, ctr, prev, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });

@@ -265,7 +265,19 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     CPD_CUDA(cudaMemcpy(plan.ent.p, ent.data(), sizeof(PlanEntry) * ent.size(), cudaMemcpyHostToDevice));
     plan.long_row.alloc(std::max(nl, 1));
     plan.long_ptr.alloc(nl + 1);
-    plan.long_ents.alloc(1);
+    // k_finish order: long rows with > FIN_SPLIT partials first (a CTA each), then the
+    // rest (a warp each)
+    {
+        const int64_t ps = warp ? 1 : GW;
+        std::vector<int32_t> order;
+        for (int32_t l = 0; l < nl; ++l)
+            if ((int64_t)(lptr[l + 1] - lptr[l]) * ps > FIN_SPLIT) order.push_back(l);
+        plan.nfin_heavy = (int32_t)order.size();
+        for (int32_t l = 0; l < nl; ++l)
+            if ((int64_t)(lptr[l + 1] - lptr[l]) * ps <= FIN_SPLIT) order.push_back(l);
+        plan.long_ents.alloc(std::max(nl, 1));
+        if (nl) CPD_CUDA(cudaMemcpy(plan.long_ents.p, order.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice));
+    }
     if (nl) CPD_CUDA(cudaMemcpy(plan.long_row.p, lrows.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice));
     CPD_CUDA(cudaMemcpy(plan.long_ptr.p, lptr.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice));
 }

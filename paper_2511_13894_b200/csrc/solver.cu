@@ -76,7 +76,7 @@ DevPlan Ctx::planA() const
     const Plan& pl = P->A.plan;
     return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
                    pl.dense_ptr.p, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortA.p, pl.long_row.p,
-                   pl.long_ptr.p, pl.long_ents.p, lpartA.p};
+                   pl.long_ptr.p, pl.long_ents.p, pl.nfin_heavy, lpartA.p};
 }
 
 DevPlan Ctx::planAT() const
@@ -84,7 +84,7 @@ DevPlan Ctx::planAT() const
     const Plan& pl = P->AT.plan;
     return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
                    pl.dense_ptr.p, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortAT.p, pl.long_row.p,
-                   pl.long_ptr.p, pl.long_ents.p, lpartAT.p};
+                   pl.long_ptr.p, pl.long_ents.p, pl.nfin_heavy, lpartAT.p};
 }
 
 void Ctx::pull_ctl()
@@ -222,7 +222,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
             if (seg.size() < 3) launch_dense();
         }
         if (dp.nlong > 0) {
-            const int gf = std::max(1, std::min(cx.P->num_sms * 8, dp.nlong));
+            const int gf = std::max(1, std::min(cx.P->num_sms * 8, std::max(dp.nfin_heavy, (dp.nlong + TPB / 32 - 1) / (TPB / 32))));
             Gate g2 = g;
             g2.active = nullptr;
             k_finish<NV, Epi><<<gf, TPB, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, prev, red);
@@ -251,7 +251,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
     CPD_CUDA(cudaGetLastError());
     ++cx.launches;
     if (dp.nlong > 0) {
-        const int gf = std::max(1, std::min(cx.P->num_sms * 8, dp.nlong));
+        const int gf = std::max(1, std::min(cx.P->num_sms * 8, std::max(dp.nfin_heavy, (dp.nlong + TPB / 32 - 1) / (TPB / 32))));
         Gate g2 = g;
         g2.active = nullptr;
         k_finish<NV, Epi><<<gf, TPB, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, gr, red);

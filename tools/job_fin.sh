@@ -1,0 +1,6 @@
+set -x
+OUT=gpurun_out/r1s2p; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || exit 1
+timeout 900 python tools/kern_time.py --config c5 --corner 1 2>&1 | tee $OUT/kt_c5.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; tail -5 $OUT/pytest_gpu.log
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --kernel-name-base demangled -k "regex:k_finish" -s 6 -c 4 python tools/prof_run.py --iters 3 > $OUT/ncu_fin.log 2>&1; grep -E "^  void|duration" $OUT/ncu_fin.log | tail -8
