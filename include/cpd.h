@@ -128,6 +128,7 @@ typedef struct {
     int64_t est_primal_pushes;  /* max(p - m, 0) */
     int64_t est_dual_pushes;    /* max(m - d, 0) */
     int32_t is_candidate;       /* candidates >= max(2m, floor) */
+    int64_t rows_eq;            /* inequality rows the corner model made '=' */
 } cpd_stats;
 
 typedef struct {
@@ -202,6 +203,16 @@ int cpd_get_kernel_times(cpd_solver *s, const char **names, double *ms, int64_t 
 int cpd_solver_counters(const cpd_solver *s, int64_t out[4]);
 /* Algorithmic bytes one launch of kernel `name` moves (DESIGN.md byte model). */
 int cpd_kernel_bytes(const cpd_solver *s, const char *name, double *bytes);
+
+/* ------------------------------------------------------------------ inequality rows
+ * Row senses ("handled implicitly"):
+ * sense[m] (GLOBAL rows, int8) 0 '=' (A_i x = b_i), 1 '<=' (A_i x <= b_i), 2 '>='.
+ * The dual step is projected onto y_i >= 0 ('>='), y_i <= 0 ('<='); the primal
+ * residual counts violations only; the corner model turns an inequality row whose
+ * slack has a non-trivial reduced cost (|y*_i| > eps_abs) into an equality
+ * (cpd_stats.rows_eq counts them).  Call before creating solvers.  CPD_E_ARG on a
+ * value outside {0, 1, 2}. */
+int cpd_problem_set_senses(cpd_problem *p, const int8_t *sense, int32_t mem);
 
 /* ------------------------------------------------------------------ preconditioning
  * Diagonal scaling of the problem (the cuPDLP+ lineage the

@@ -32,7 +32,7 @@ DECLARED_SYMBOLS = [
     "cpd_get_trajectory", "cpd_power_sigma", "cpd_problem_score", "cpd_compute_stats",
     "cpd_get_kernel_times", "cpd_kernel_bytes", "cpd_solver_counters",
     "cpd_partition", "cpd_nccl_get_unique_id", "cpd_problem_create_dist", "cpd_problem_dist_info",
-    "cpd_problem_scale", "cpd_problem_get_scaling",
+    "cpd_problem_scale", "cpd_problem_get_scaling", "cpd_problem_set_senses",
 ]
 
 
@@ -61,7 +61,7 @@ class Result(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(k, C.c_int64) for k in ("off_bound", "off_bound_strict", "off_bound_model", "zero_rc",
                                          "candidates", "fix_lb", "fix_ub", "est_primal_pushes",
-                                         "est_dual_pushes")] + [("is_candidate", C.c_int32)]
+                                         "est_dual_pushes")] + [("is_candidate", C.c_int32), ("rows_eq", C.c_int64)]
 
 
 class CornerParams(C.Structure):
@@ -118,6 +118,7 @@ def lib():
                                                   P, I32, C.POINTER(P)]),
             "cpd_problem_dist_info": (C.c_int, [P, P]),
             "cpd_problem_scale": (C.c_int, [P, I32, I32]),
+            "cpd_problem_set_senses": (C.c_int, [P, P, I32]),
             "cpd_problem_get_scaling": (C.c_int, [P, P, P]),
         }
         for name, (res, args) in sig.items():
@@ -231,7 +232,10 @@ class Problem:
             AT = tuple(conv(a) for a in AT)
             A = tuple(conv(a) for a in A) if A else None
             vecs = {k: conv(v) for k, v in vecs.items()}
-        return cls(lp.m, lp.n, A=A, AT=AT, device=device, **vecs)
+        P = cls(lp.m, lp.n, A=A, AT=AT, device=device, **vecs)
+        if getattr(lp, "sense", None) is not None:
+            P.set_senses(lp.sense)
+        return P
 
     @classmethod
     def create_dist(cls, lp, rank, world, uid: bytes, partition=-1, device=0):
@@ -249,6 +253,14 @@ class Problem:
         self.h = h
         self.nnz = int(lp.ATp[-1])
         self.mem = HOST
+        if getattr(lp, "sense", None) is not None:
+            self.set_senses(lp.sense)
+        return self
+
+    def set_senses(self, sense):
+        """cpd_problem_set_senses: int8 row senses (0 '=', 1 '<=', 2 '>='), global rows."""
+        a = np.ascontiguousarray(sense, dtype=np.int8)
+        _check(lib().cpd_problem_set_senses(self.h, a.ctypes.data, HOST))
         return self
 
     def scale(self, ruiz_iters=10, pock_chambolle=1):

@@ -134,6 +134,10 @@ struct cpd_problem {
     int64_t L = 0;                   // slice length of the split side
     std::vector<int64_t> rank_gofs[2], rank_len[2];   // every rank's owned part (global)
     void* comm = nullptr;            // ncclComm_t (split >= 0)
+    // ---- row senses (cpd_problem_set_senses; NEXT-2): local rows of A, null = all '='
+    cpd::DBuf<int8_t> sense;
+    bool has_sense = false;
+    const int8_t* sense_own() const { return has_sense ? sense.p + poff[0] : nullptr; }
     // ---- diagonal preconditioning (cpd_problem_scale; R-3): the device LP is
     // the scaled one (A^ = diag(r) A diag(s), b^ = r b, c^ = s c, l^ = l/s, u^ = u/s);
     // sr = r, ss = s, ir = 1/r, is = 1/s; lb0/ub0 the original bounds.  Unscaled: nulls.

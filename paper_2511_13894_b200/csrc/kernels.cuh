@@ -234,6 +234,22 @@ __device__ __forceinline__ void dual_terms(double z, double lo, double hi, doubl
     rd2 += rd * rd;
 }
 
+// Implicit inequality rows: sense 0 '=', 1 '<=' (Ax <= b),
+// 2 '>=' (Ax >= b).  r = b - Ax counts its violation only; the dual of L = c^T x +
+// y^T (b - A x) is projected onto y >= 0 ('>=') / y <= 0 ('<=').
+__device__ __forceinline__ double row_viol(const int8_t* sn, int i, double r)
+{
+    if (!sn) return r;
+    const int s = sn[i];
+    return s == 1 ? (r < 0.0 ? r : 0.0) : s == 2 ? (r > 0.0 ? r : 0.0) : r;
+}
+__device__ __forceinline__ double dual_proj(const int8_t* sn, int i, double v)
+{
+    if (!sn) return v;
+    const int s = sn[i];
+    return s == 1 ? (v < 0.0 ? v : 0.0) : s == 2 ? (v > 0.0 ? v : 0.0) : v;
+}
+
 // ------------------------------------------------------------ reductions
 template <int NS>
 __device__ __forceinline__ void warp_sum(double (&v)[NS])
@@ -1399,6 +1415,7 @@ struct EpiDual {
     double *y, *ya, *ax;
     double sigma, inv_t;
     const double* w = nullptr;   // 1/r (scaled problem): ||r_P|| in the original space
+    const int8_t* sn = nullptr;  // row senses (null: all equality rows)
     __device__ void load(const Ctl* ctl)
     {
         sigma = ctl->sigma;
@@ -1414,12 +1431,12 @@ struct EpiDual {
         const double axn = s[0];
         const double bi = vin[0][li];
         const double yo = vin[1][li];
-        const double yp = yo + sigma * (bi - (2.0 * axn - vin[2][li]));
+        const double yp = dual_proj(sn, i, yo + sigma * (bi - (2.0 * axn - vin[2][li])));
         y[i] = yp;
         ax[i] = axn;
         const double yav = vin[3][li];
         __stcs(&ya[i], yav + (yp - yav) * inv_t);
-        const double r = (bi - axn) * (w ? w[i] : 1.0);
+        const double r = row_viol(sn, i, bi - axn) * (w ? w[i] : 1.0);
         acc[0] += r * r;
         acc[1] += bi * yp;
         acc[2] += isfinite(yp) ? 0.0 : 1.0;
@@ -1498,12 +1515,13 @@ struct EpiCheckM {
     const double *b, *y, *ya, *yr;
     double* axa;
     const double* w = nullptr;   // 1/r (scaled problem)
+    const int8_t* sn = nullptr;  // row senses
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ void row(int i, const double* s, const double* const*, int, double* acc) const
     {
         axa[i] = s[0];
         const double bi = b[i];
-        const double r = (bi - s[0]) * (w ? w[i] : 1.0);
+        const double r = row_viol(sn, i, bi - s[0]) * (w ? w[i] : 1.0);
         acc[0] += r * r;
         const double yav = ya[i], yo = y[i], yri = yr[i];
         acc[1] += bi * yav;
@@ -1678,11 +1696,12 @@ struct EpiInitM {
     const double *b, *y;
     double* ax;   // may be null (score only)
     const double* w = nullptr;   // 1/r (scaled problem)
+    const int8_t* sn = nullptr;  // row senses
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ void row(int i, const double* s, const double* const*, int, double* acc) const
     {
         if (ax) ax[i] = s[0];
-        const double r = (b[i] - s[0]) * (w ? w[i] : 1.0);
+        const double r = row_viol(sn, i, b[i] - s[0]) * (w ? w[i] : 1.0);
         acc[0] += r * r;
         acc[1] += b[i] * y[i];
     }
@@ -1811,6 +1830,29 @@ struct EpiCorner {
         ctl->out[0] = tot[0];
         ctl->out[1] = tot[1];
     }
+};
+
+// Corner-model row senses: an inequality row whose slack has a
+// non-trivial reduced cost (|y*_i| > eps_abs, y* in the original space) becomes an
+// equality; counts the changed rows.
+struct OpSense {
+    static constexpr int NS = 1;
+    const int8_t* sn;
+    const double* y;
+    const double* sy;   // r (scaled problem): y = r y^
+    int8_t* shat;
+    double eps;
+    __device__ void load(const Ctl*) {}
+    __device__ __forceinline__ void elem(int64_t ii, double* acc) const
+    {
+        const int i = (int)ii;
+        const int s = sn[i];
+        const double yo = sy ? y[i] * sy[i] : y[i];
+        const bool eq = s != 0 && fabs(yo) > eps;
+        shat[i] = eq ? (int8_t)0 : (int8_t)s;
+        acc[0] += eq ? 1.0 : 0.0;
+    }
+    __device__ void finalize(const double* tot, Ctl* ctl) const { ctl->out[2] = tot[0]; }
 };
 
 // a10 corner statistics: counts as exact fp64 sums (< 2^53).

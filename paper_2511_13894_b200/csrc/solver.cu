@@ -372,7 +372,7 @@ struct Reps {
 // Standalone evaluations shared by the solver and the stand-alone ABI calls.
 // score of (x, y) (owned parts) for objective c / bounds bd (owned parts)
 static void eval_score(Ctx& cx, const double* x, const double* y, const double* c, Bounds bd,
-                       double nb, double nc, double out[8])
+                       double nb, double nc, double out[8], const int8_t* sn = nullptr)
 {
     AuxScope aux(cx);
     const cpd_problem* P = cx.P;
@@ -384,6 +384,7 @@ static void eval_score(Ctx& cx, const double* x, const double* y, const double* 
     cx.push_ctl(h);
     EpiInitM em{P->b_own(), y, nullptr};
     em.w = P->w_m();
+    em.sn = sn;
     pass<1>(cx, 0, fixed(rp.view(cx, 1, x)), none(), em, always());
     EpiInitN en{c, x, bd, 0};
     en.w = P->w_n();
@@ -436,6 +437,7 @@ static void eval_stats(Ctx& cx, bool internal, const double* x, const double* z,
     out->candidates = z ? (int64_t)o[4] : 0;
     out->fix_lb = fix_lb;
     out->fix_ub = fix_ub;
+    out->rows_eq = 0;
     const int64_t m = P->m_glob;
     out->est_primal_pushes = std::max<int64_t>(out->off_bound - m, 0);
     out->est_dual_pushes = z ? std::max<int64_t>(m - out->zero_rc, 0) : 0;
@@ -540,6 +542,8 @@ struct cpd_solver {
     // state vectors: n-side (x-like) of length own_len[1], m-side (y-like) own_len[0]
     DBuf<double> X0, X1, Xa0, Xa1, Xr, Y, Ya, Yr, AX, AXa, Ystar, Z, lhat, uhat, chat, objd, SN, SM;
     DBuf<double> LHo, UHo, TX, TY;   // scaled problems: original-space model bounds; unscale scratch
+    DBuf<int8_t> shat;                // corner-model row senses
+    int64_t rows_eq = 0;
     // replicas of the split side (world * L): current vector / its average
     DBuf<double> RV, RA;
     DBuf<int64_t> trk, troff;
@@ -605,6 +609,7 @@ struct cpd_solver {
         for (auto e : ev1) cudaEventDestroy(e);
         if (h_active) cudaFreeHost(h_active);
     }
+    const int8_t* sense_of(int kind) const { return kind ? (P->has_sense ? shat.p : nullptr) : P->sense_own(); }
     const double* lh_orig() const { return P->scaled ? LHo.p : lhat.p; }
     const double* uh_orig() const { return P->scaled ? UHo.p : uhat.p; }
     int32_t nO() const { return P->own_len[1]; }
@@ -658,6 +663,7 @@ struct cpd_solver {
         elem(cx, std::max(n, m), ob, always(), false);
         EpiInitM em{P->b_own(), Y.p, AX.p};
         em.w = P->w_m();
+        em.sn = sense_of(rc.kind);
         pass<1>(cx, 0, fixed(rp.view(cx, 1, X0.p)), none(), em, always());
         EpiInitN en{c, X0.p, bd, 1};
         en.w = P->w_n();
@@ -705,6 +711,7 @@ struct cpd_solver {
             rec(ev1, NODE_CHECK_N);
             EpiCheckM em{P->b_own(), Y.p, Ya.p, Yr.p, AXa.p};
             em.w = P->w_m();
+            em.sn = sense_of(kind);
             Gate gm{GATE_CHECK, 0, NODE_CHECK_M, active.p};
             rec(ev0, NODE_CHECK_M);
             refresh(cx, 1, VecSel{Xa0.p, Xa1.p, 2}, RA.p, gm);
@@ -737,6 +744,7 @@ struct cpd_solver {
             rec(ev1, n1);
             EpiDual e2{P->b_own(), Y.p, Ya.p, AX.p, 0.0, 0.0};
             e2.w = P->w_m();
+            e2.sn = sense_of(kind);
             rec(ev0, n2);
             pass<1>(cx, 0, gsrc(1, VecSel{X0.p, X1.p, 1}, RV.p), none(), e2, g2);
             // y_{k+1} replica for the next primal step (split m-side); k already advanced
@@ -838,7 +846,7 @@ struct cpd_solver {
     {
         const Ctl h = *cx.h_ctl;   // state at termination
         double o[8];
-        eval_score(cx, Xp(cur_par), Y.p, obj_of(kind), bounds_of(kind), h.nb, h.nc, o);
+        eval_score(cx, Xp(cur_par), Y.p, obj_of(kind), bounds_of(kind), h.nb, h.nc, o, sense_of(kind));
         r->status = h.status;
         r->returned_average = h.returned_average;
         r->iterations = (h.status == ST_RUNNING) ? h.k : h.iterations;
@@ -935,14 +943,23 @@ struct cpd_solver {
                 ec.ob = P->bounds_orig();
             }
             pass<1>(cx, 1, fixed(rp.view(cx, 0, Ystar.p)), none(), ec, always());
+            rows_eq = 0;
+            if (P->has_sense) {   // inequality rows with |y*_i| > eps_abs become '='
+                if (!shat.p) shat.alloc(std::max(m, 1));
+                OpSense os{P->sense_own(), Ystar.p, P->scaled ? P->sr.p : nullptr, shat.p, cp.eps_abs};
+                elem(cx, m, os, always(), true);
+            }
             cx.pull_ctl();
             fix_lb = (int64_t)cx.h_ctl->out[0];
             fix_ub = (int64_t)cx.h_ctl->out[1];
+            if (P->has_sense) rows_eq = (int64_t)cx.h_ctl->out[2];
         }
         have_corner = true;
-        if (before)
+        if (before) {
             eval_stats(cx, true, Xp(cur_par), Z.p, lh_orig(), uh_orig(), cp.eps_abs, cp.candidate_floor, fix_lb,
                        fix_ub, before);
+            before->rows_eq = rows_eq;
+        }
         if (!eta_known) {
             // no phase 1 on this solver: step size as phase 1 would have chosen it
             if (prm.step_size > 0.0) eta_phase1 = prm.step_size;
@@ -970,9 +987,11 @@ struct cpd_solver {
         k_copy<<<g, 256, 0, cx.st>>>(m, Y.p, Ystar.p);
         CPD_CUDA(cudaGetLastError());
         ++cx.launches;
-        if (after)
+        if (after) {
             eval_stats(cx, true, Xp(cur_par), Z.p, lh_orig(), uh_orig(), cp.eps_abs, cp.candidate_floor, fix_lb,
                        fix_ub, after);
+            after->rows_eq = rows_eq;
+        }
     }
 
     // x: n-side vector, y: m-side vector, both GLOBAL length; each rank takes its part.
@@ -1121,6 +1140,24 @@ int cpd_problem_create_dist(int32_t rank, int32_t world, const char id[128], int
     if (!out) return fail(CPD_E_ARG, "out is NULL");
     *out = cpd_problem_create_dist_impl(rank, world, id, partition, m, n, nnz, AT_rowptr, AT_col, AT_val, b, c,
                                         lb, ub, device);
+    ABI_END
+}
+
+int cpd_problem_set_senses(cpd_problem* p, const int8_t* sense, int32_t mem)
+{
+    ABI_BEGIN
+    if (!p || !sense) return fail(CPD_E_ARG, "NULL argument");
+    // this rank's local rows of A: all m (single GPU, col-block) or rows R_p (row-block)
+    const int64_t off = p->split == 1 ? p->gofs[0] : 0;
+    std::vector<int8_t> h((size_t)p->m);
+    if (mem == CPD_DEVICE) CPD_CUDA(cudaMemcpy(h.data(), sense + off, (size_t)p->m, cudaMemcpyDeviceToHost));
+    else std::memcpy(h.data(), sense + off, (size_t)p->m);
+    for (int64_t i = 0; i < p->m; ++i)
+        if (h[i] < 0 || h[i] > 2) return fail(CPD_E_ARG, "row sense must be 0, 1 or 2 (row " + std::to_string(i + off) + ")");
+    CPD_CUDA(cudaSetDevice(p->device));
+    p->sense.alloc(std::max<int32_t>(p->m, 1));
+    CPD_CUDA(cudaMemcpy(p->sense.p, h.data(), (size_t)p->m, cudaMemcpyHostToDevice));
+    p->has_sense = true;
     ABI_END
 }
 
@@ -1326,6 +1363,7 @@ int cpd_get_stats(const cpd_solver* cs, int64_t candidate_floor, cpd_stats* out)
     eval_stats(s->cx, true, s->Xp(s->cur_par), s->Z.p, s->have_corner ? s->lh_orig() : nullptr,
                s->have_corner ? s->uh_orig() : nullptr, s->have_corner ? s->corner_eps : s->prm.eps_abs,
                candidate_floor, s->have_corner ? s->fix_lb : 0, s->have_corner ? s->fix_ub : 0, out);
+    out->rows_eq = s->have_corner ? s->rows_eq : 0;
     ABI_END
 }
 
@@ -1378,7 +1416,7 @@ int cpd_problem_score(const cpd_problem* p, const double* x, const double* y, in
     }
     double nb, nc;
     eval_norms(cx, p->b_own(), p->c_own(), &nb, &nc);
-    eval_score(cx, dx.p, dy.p, p->c_own(), p->bounds_own(), nb, nc, out);
+    eval_score(cx, dx.p, dy.p, p->c_own(), p->bounds_own(), nb, nc, out, p->sense_own());
     ABI_END
 }
 
