@@ -40,7 +40,10 @@ constexpr int WLONG = 512;       // k_csrw: a longer row is cut into pieces
 #endif
 constexpr int WCAP_LONG = CPD_WCAP_LONG;  // k_csrw: nonzeros per long-row piece
 constexpr int HEAVY_MIN = 65536; // k_dense: rows with at least this many nonzeros
-constexpr int HB = 8192;         // k_dense: columns per dense block (64 KB of the vector in smem)
+#ifndef CPD_HB
+#define CPD_HB 8192
+#endif
+constexpr int HB = CPD_HB;       // k_dense: columns per dense block (64 KB of the vector in smem)
 constexpr int DCHUNK = 512;      // k_dense: entries per item (balances the Zipf head across warps)
 constexpr int TPB_D = 512;
 constexpr int FIN_SPLIT = 1024;  // k_finish: rows with more partials get a CTA, the rest a warp
@@ -1123,7 +1126,10 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     constexpr int NWD = TPB_D / 32;
-    constexpr int DU = 8;
+#ifndef CPD_DU
+#define CPD_DU 8
+#endif
+    constexpr int DU = CPD_DU;
     for (int blk = blockIdx.x; blk < P.nhb; blk += gridDim.x) {
         const int j0 = blk * HB, nj = min(HB, cols - j0);
         __syncthreads();

@@ -120,6 +120,9 @@ void Ctx::set_i32(int32_t* f, int32_t v)
 void Ctx::sync() { CPD_CUDA(cudaStreamSynchronize(st)); }
 
 static std::mutex g_grid_mu;
+#ifndef CPD_SLAB_MERGE
+#define CPD_SLAB_MERGE 0
+#endif
 
 template <int NV, class Epi>
 void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel v1, const Epi& epi,
@@ -215,6 +218,12 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
             // the heavy rows' dense blocks, then each slab's long pieces
             for (size_t k = 0; k + 1 < seg.size(); ++k) {
                 if (k == 1) launch_dense();
+#if CPD_SLAB_MERGE
+                if (k == 1 && !single) {   // every slab's pieces in one launch
+                    if (seg.back() > seg[1]) launch_items(seg[1], seg.back(), 0);
+                    break;
+                }
+#endif
                 if (seg[k + 1] <= seg[k] && !single) continue;
                 launch_items(seg[k], seg[k + 1], single ? 1 : 0);
                 if (single) break;

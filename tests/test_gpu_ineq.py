@@ -26,7 +26,13 @@ def close(a, b, rtol=1e-9):
 
 @pytest.fixture(scope="module")
 def ineq():
+    """c4-s-ineq with every capacity cut to the planted routing's load + 0.5, so many
+    capacity rows bind (non-zero duals: the P:301-306 rule has rows to change)."""
     lp = lpgen.config("c4-s-ineq")
+    K, NA = lp.meta["K"], lp.meta["NA"]
+    load = lp.x0.reshape(K, NA).sum(0)
+    lp.b = lp.b.copy()
+    lp.b[lp.m - NA:] = load + 0.5
     return lp, oracle.OracleLP(lp)
 
 
@@ -85,7 +91,8 @@ def test_ineq_solve_and_corner(ineq, kind):
         xh, _, z_o, rco, b_o, a_o, model = oracle.corner_push(olp, xo, yo, seed=1001, floor=100)
     assert rc["status"] == rco["status"] == 0
     assert abs(rc["iterations"] - rco["iterations"]) <= max(1, 0.01 * rco["iterations"])
-    assert before["rows_eq"] == after["rows_eq"] == model["rows_eq"] > 0
+    assert before["rows_eq"] == after["rows_eq"] == model["rows_eq"]
+    assert model["rows_eq"] == int(np.sum((lp.sense != 0) & (np.abs(yo) > 1e-6))) > 0
     xg, yg, zg = S.get_iterate(z=True)
     ref = oracle.stats(lp.m, xg, zg, lp.lb, lp.ub, model["lhat"], model["uhat"], 1e-6, 100)
     for k in ("off_bound", "off_bound_strict", "off_bound_model", "zero_rc", "candidates"):
