@@ -71,6 +71,7 @@ struct Plan {
     int32_t nheavy = 0, nhb = 0;          // heavy rows (k_dense) and column blocks of HB
     DBuf<PlanEntry> dense_ent;            // {slot, block, q0, q1} grouped by block
     DBuf<int32_t> dense_ptr;              // [nhb + 1] item range of each block
+    int32_t dense_maxitems = 0;           // most items in one block (k_dense smem)
     // short rows by column slab (k_short): [nslab][rows + 1] pointers, entries slab-major
     int32_t short_on = 0;
     int64_t short_nnz = 0;

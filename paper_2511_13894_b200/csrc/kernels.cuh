@@ -67,6 +67,7 @@ struct DevPlan {
     int32_t nheavy, nhb;       // heavy rows / dense column blocks (k_dense)
     const PlanEntry* dense_ent;   // {slot, block, q0, q1}: <= DCHUNK entries of one heavy row in one block
     const int32_t* dense_ptr;     // [nhb + 1] items of each block
+    int32_t dense_maxitems;       // most items in one block (k_dense item-sum smem)
     const int32_t* short_ptr;     // [nslab][rows + 1] short-row entries by slab (k_short)
     const int32_t* short_col;
     const double* short_val;
@@ -1116,11 +1117,12 @@ template <int NV>
 __global__ void __launch_bounds__(TPB_D)
 k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ctl* ctl)
 {
-    extern __shared__ __align__(16) double xs[];   // [NV][HB]
+    extern __shared__ __align__(16) double xs[];   // [NV][HB] vector block, then [NV][maxitems] item sums
     __shared__ int s_go;
     if (threadIdx.x == 0) s_go = gate_open(gate, ctl);
     __syncthreads();
     if (!s_go) return;
+    double* isum = xs + NV * HB;
     const double* __restrict__ v0 = vs0.get(ctl);
     const double* __restrict__ v1 = vs1.get(ctl);
     const unsigned FULL = 0xffffffffu;
@@ -1132,14 +1134,14 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
     constexpr int DU = CPD_DU;
     for (int blk = blockIdx.x; blk < P.nhb; blk += gridDim.x) {
         const int j0 = blk * HB, nj = min(HB, cols - j0);
+        const int i0 = P.dense_ptr[blk], i1 = P.dense_ptr[blk + 1], ni = i1 - i0;
         __syncthreads();
         for (int t = threadIdx.x; t < nj; t += TPB_D) {
             xs[t] = v0[j0 + t];
             if (NV > 1) xs[HB + t] = v1[j0 + t];
         }
         __syncthreads();
-        const int i1 = P.dense_ptr[blk + 1];
-        for (int i = P.dense_ptr[blk] + w; i < i1; i += NWD) {
+        for (int i = i0 + w; i < i1; i += NWD) {
             const PlanEntry E = P.dense_ent[i];
             double sm[NV];
 #pragma unroll
@@ -1167,7 +1169,22 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
                 for (int o = 16; o > 0; o >>= 1) sm[v] += __shfl_xor_sync(FULL, sm[v], o);
             if (lane == 0)
 #pragma unroll
-                for (int v = 0; v < NV; ++v) P.lpart[(size_t)E.a * 2 + v] = sm[v];
+                for (int v = 0; v < NV; ++v) isum[v * P.dense_maxitems + (i - i0)] = sm[v];
+        }
+        __syncthreads();
+        // one partial per (row, block): the thread of a group's first item sums the
+        // group's item sums in item order (fixed: deterministic)
+        for (int k = threadIdx.x; k < ni; k += TPB_D) {
+            const int slot = P.dense_ent[i0 + k].a;
+            if (k > 0 && P.dense_ent[i0 + k - 1].a == slot) continue;
+            double tot[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) tot[v] = 0.0;
+            for (int kk = k; kk < ni && P.dense_ent[i0 + kk].a == slot; ++kk)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) tot[v] += isum[v * P.dense_maxitems + kk];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) P.lpart[(size_t)slot * 2 + v] = tot[v];
         }
     }
 }

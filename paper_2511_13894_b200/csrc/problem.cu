@@ -173,7 +173,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
             int64_t cnt = 0;
             for (int32_t b = 0; b < nhb; ++b) {
                 const int64_t len = (int64_t)hpos[(size_t)h * (nhb + 1) + b + 1] - hpos[(size_t)h * (nhb + 1) + b];
-                cnt += (len + DCHUNK - 1) / DCHUNK;
+                cnt += len > 0 ? 1 : 0;   // one partial slot per non-empty (row, block)
             }
             lptr[heavy_l[h] + 1] = (int32_t)cnt;
         }
@@ -183,20 +183,26 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     plan.nhb = nhb;
     if (nh > 0) {
         std::vector<std::vector<PlanEntry>> dl(nhb);
+        // items of one (row, block) share its slot and are consecutive in the block's list
         for (int32_t h = 0; h < nh; ++h) {
             int32_t slot = lptr[heavy_l[h]];
             for (int32_t b = 0; b < nhb; ++b) {
                 const int32_t q0 = hpos[(size_t)h * (nhb + 1) + b], q1 = hpos[(size_t)h * (nhb + 1) + b + 1];
+                if (q1 <= q0) continue;
                 for (int32_t q = q0; q < q1; q += DCHUNK)
-                    dl[b].push_back(PlanEntry{slot++, b, q, std::min(q + DCHUNK, q1)});
+                    dl[b].push_back(PlanEntry{slot, b, q, std::min(q + DCHUNK, q1)});
+                ++slot;
             }
         }
         std::vector<PlanEntry> dent;
         std::vector<int32_t> dptr(nhb + 1, 0);
+        int32_t maxit = 1;
         for (int32_t b = 0; b < nhb; ++b) {
             dent.insert(dent.end(), dl[b].begin(), dl[b].end());
             dptr[b + 1] = (int32_t)dent.size();
+            maxit = std::max<int32_t>(maxit, (int32_t)dl[b].size());
         }
+        plan.dense_maxitems = maxit;
         plan.dense_ent.alloc(std::max<size_t>(dent.size(), 1));
         plan.dense_ptr.alloc(nhb + 1);
         CPD_CUDA(cudaMemcpy(plan.dense_ent.p, dent.data(), sizeof(PlanEntry) * dent.size(), cudaMemcpyHostToDevice));

@@ -75,7 +75,7 @@ DevPlan Ctx::planA() const
 {
     const Plan& pl = P->A.plan;
     return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
-                   pl.dense_ptr.p, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortA.p, pl.long_row.p,
+                   pl.dense_ptr.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortA.p, pl.long_row.p,
                    pl.long_ptr.p, pl.long_ents.p, pl.nfin_heavy, lpartA.p};
 }
 
@@ -83,7 +83,7 @@ DevPlan Ctx::planAT() const
 {
     const Plan& pl = P->AT.plan;
     return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
-                   pl.dense_ptr.p, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortAT.p, pl.long_row.p,
+                   pl.dense_ptr.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortAT.p, pl.long_row.p,
                    pl.long_ptr.p, pl.long_ents.p, pl.nfin_heavy, lpartAT.p};
 }
 
@@ -121,7 +121,7 @@ void Ctx::sync() { CPD_CUDA(cudaStreamSynchronize(st)); }
 
 static std::mutex g_grid_mu;
 #ifndef CPD_SLAB_MERGE
-#define CPD_SLAB_MERGE 0
+#define CPD_SLAB_MERGE 1
 #endif
 
 template <int NV, class Epi>
@@ -166,16 +166,18 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         Gate gs = g;
         auto launch_dense = [&]() {
             if (dp.nheavy > 0) {   // heavy rows by dense column blocks (their slots, then k_finish)
-                constexpr size_t DSM = (size_t)NV * HB * sizeof(double);
+                const size_t DSM = (size_t)NV * (HB + dp.dense_maxitems) * sizeof(double);
                 static int dgrid = 0, dsms = 0;
+                static size_t dsm_set = 0;
                 {
                     std::lock_guard<std::mutex> lk(g_grid_mu);
-                    if (!dgrid || dsms != cx.P->num_sms) {
+                    if (!dgrid || dsms != cx.P->num_sms || dsm_set != DSM) {
                         CPD_CUDA(cudaFuncSetAttribute(k_dense<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       (int)DSM));
                         int nb = 0;
                         CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dense<NV>, TPB_D, DSM));
                         dsms = cx.P->num_sms;
+                        dsm_set = DSM;
                         dgrid = std::max(1, nb) * dsms;
                     }
                 }
