@@ -74,6 +74,8 @@ struct Plan {
     int32_t dense_maxitems = 0;           // most items in one block (k_dense smem)
     // short rows by column slab (k_short): [nslab][rows + 1] pointers, entries slab-major
     int32_t short_on = 0;
+    int32_t short_nslab = 1;
+    int64_t short_width = 0;
     int64_t short_nnz = 0;
     DBuf<int32_t> short_ptr, short_col;
     DBuf<double> short_val;

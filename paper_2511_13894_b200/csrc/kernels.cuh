@@ -769,9 +769,25 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
 #pragma unroll
         for (int v = 0; v < NV; ++v) sm[v] = 0.0;
         const int64_t t0 = (int64_t)P.long_ptr[l] * P.pslot, t1 = (int64_t)P.long_ptr[l + 1] * P.pslot;
-        for (int64_t t = t0 + threadIdx.x; t < t1; t += TPB)
+        // 8 independent accumulators per thread (loads in flight), combined in fixed order
+        double a8[8][NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) sm[v] += __ldcg(&P.lpart[t * 2 + v]);
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) a8[u][v] = 0.0;
+        int64_t t = t0 + threadIdx.x;
+        for (; t + 7 * TPB < t1; t += 8 * TPB)
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) a8[u][v] += __ldcg(&P.lpart[(t + u * TPB) * 2 + v]);
+        for (int u = 0; t < t1; t += TPB, ++u)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) a8[u & 7][v] += __ldcg(&P.lpart[t * 2 + v]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) sm[v] += a8[u][v];
         block_sum<NV>(sm, s_w);
         if (threadIdx.x == 0) {
             const int r = P.long_row[l];
@@ -1117,12 +1133,11 @@ template <int NV>
 __global__ void __launch_bounds__(TPB_D)
 k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ctl* ctl)
 {
-    extern __shared__ __align__(16) double xs[];   // [NV][HB] vector block, then [NV][maxitems] item sums
+    extern __shared__ __align__(16) double xs[];   // [NV][HB] vector block
     __shared__ int s_go;
     if (threadIdx.x == 0) s_go = gate_open(gate, ctl);
     __syncthreads();
     if (!s_go) return;
-    double* isum = xs + NV * HB;
     const double* __restrict__ v0 = vs0.get(ctl);
     const double* __restrict__ v1 = vs1.get(ctl);
     const unsigned FULL = 0xffffffffu;
@@ -1134,7 +1149,7 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
     constexpr int DU = CPD_DU;
     for (int blk = blockIdx.x; blk < P.nhb; blk += gridDim.x) {
         const int j0 = blk * HB, nj = min(HB, cols - j0);
-        const int i0 = P.dense_ptr[blk], i1 = P.dense_ptr[blk + 1], ni = i1 - i0;
+        const int i0 = P.dense_ptr[blk], i1 = P.dense_ptr[blk + 1];
         __syncthreads();
         for (int t = threadIdx.x; t < nj; t += TPB_D) {
             xs[t] = v0[j0 + t];
@@ -1169,22 +1184,7 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
                 for (int o = 16; o > 0; o >>= 1) sm[v] += __shfl_xor_sync(FULL, sm[v], o);
             if (lane == 0)
 #pragma unroll
-                for (int v = 0; v < NV; ++v) isum[v * P.dense_maxitems + (i - i0)] = sm[v];
-        }
-        __syncthreads();
-        // one partial per (row, block): the thread of a group's first item sums the
-        // group's item sums in item order (fixed: deterministic)
-        for (int k = threadIdx.x; k < ni; k += TPB_D) {
-            const int slot = P.dense_ent[i0 + k].a;
-            if (k > 0 && P.dense_ent[i0 + k - 1].a == slot) continue;
-            double tot[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) tot[v] = 0.0;
-            for (int kk = k; kk < ni && P.dense_ent[i0 + kk].a == slot; ++kk)
-#pragma unroll
-                for (int v = 0; v < NV; ++v) tot[v] += isum[v * P.dense_maxitems + kk];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) P.lpart[(size_t)slot * 2 + v] = tot[v];
+                for (int v = 0; v < NV; ++v) P.lpart[(size_t)E.a * 2 + v] = sm[v];
         }
     }
 }

@@ -19,6 +19,9 @@ namespace cpd {
 // Column slab width for long-row pieces: 4M columns = 32 MB of the gathered fp64
 // vector, so the slab being swept stays resident in the 126 MB L2.
 constexpr int64_t SLAB_COLS = 4 << 20;
+#ifndef CPD_SHORT_SLABS
+#define CPD_SHORT_SLABS 2   // short rows (CPD_SHORT=1): column slabs of n / 2 (80 MB of C5's x each)
+#endif
 
 // pos[l * nb + s - 1] = first position q of long row l with col[q] >= s * SLAB_COLS.
 __global__ void k_slab_pos(int32_t nl, int32_t nb, const int32_t* lrows, const int32_t* p,
@@ -41,19 +44,19 @@ __global__ void k_slab_pos(int32_t nl, int32_t nb, const int32_t* lrows, const i
 // Short rows (<= long_min entries) split by column slab: cnt[s * rows + r] = entries of
 // row r in slab s (0 for long rows).
 __global__ void k_short_count(int32_t rows, int32_t nslab, int64_t long_min, const int32_t* p, const int32_t* col,
-                              int32_t* cnt)
+                              int32_t* cnt, int64_t width)
 {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
         const int32_t a = p[r], b = p[r + 1];
         for (int32_t s = 0; s < nslab; ++s) cnt[(int64_t)s * rows + r] = 0;
         if (b - a > long_min) continue;
-        for (int32_t q = a; q < b; ++q) cnt[(int64_t)(col[q] / SLAB_COLS) * rows + r] += 1;
+        for (int32_t q = a; q < b; ++q) cnt[(int64_t)(col[q] / width) * rows + r] += 1;
     }
 }
 
 // entries copied slab-major (row order, then column order inside each slab)
 __global__ void k_short_fill(int32_t rows, int32_t nslab, int64_t long_min, const int32_t* p, const int32_t* col,
-                             const double* val, const int32_t* sp, int32_t* scol, double* sval)
+                             const double* val, const int32_t* sp, int32_t* scol, double* sval, int64_t width)
 {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
         const int32_t a = p[r], b = p[r + 1];
@@ -61,7 +64,7 @@ __global__ void k_short_fill(int32_t rows, int32_t nslab, int64_t long_min, cons
         int32_t q = a;
         for (int32_t s = 0; s < nslab; ++s) {
             int32_t d = sp[(int64_t)s * (rows + 1) + r];
-            while (q < b && col[q] / SLAB_COLS == s) {
+            while (q < b && col[q] / width == s) {
                 scol[d] = col[q];
                 sval[d] = val[q];
                 ++d;
@@ -173,7 +176,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
             int64_t cnt = 0;
             for (int32_t b = 0; b < nhb; ++b) {
                 const int64_t len = (int64_t)hpos[(size_t)h * (nhb + 1) + b + 1] - hpos[(size_t)h * (nhb + 1) + b];
-                cnt += len > 0 ? 1 : 0;   // one partial slot per non-empty (row, block)
+                cnt += (len + DCHUNK - 1) / DCHUNK;   // one partial slot per item
             }
             lptr[heavy_l[h] + 1] = (int32_t)cnt;
         }
@@ -183,15 +186,12 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     plan.nhb = nhb;
     if (nh > 0) {
         std::vector<std::vector<PlanEntry>> dl(nhb);
-        // items of one (row, block) share its slot and are consecutive in the block's list
         for (int32_t h = 0; h < nh; ++h) {
             int32_t slot = lptr[heavy_l[h]];
             for (int32_t b = 0; b < nhb; ++b) {
                 const int32_t q0 = hpos[(size_t)h * (nhb + 1) + b], q1 = hpos[(size_t)h * (nhb + 1) + b + 1];
-                if (q1 <= q0) continue;
                 for (int32_t q = q0; q < q1; q += DCHUNK)
-                    dl[b].push_back(PlanEntry{slot, b, q, std::min(q + DCHUNK, q1)});
-                ++slot;
+                    dl[b].push_back(PlanEntry{slot++, b, q, std::min(q + DCHUNK, q1)});
             }
         }
         std::vector<PlanEntry> dent;
@@ -234,10 +234,15 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     // 453 us rows segment, profiles/r01_kernel_iterations.md v18); CPD_SHORT=1 enables.
     plan.short_on = 0;
     const char* she = getenv("CPD_SHORT");
+    const int32_t nss = (int32_t)std::min<int64_t>(CPD_SHORT_SLABS, std::max<int64_t>(1, cols));
+    const int64_t sw = ((int64_t)cols + nss - 1) / nss;
+    plan.short_nslab = nss;
+    plan.short_width = sw;
     if (warp && nslab >= 2 && rows > 0 && she && she[0] == '1') {
+        const int32_t nslab = nss;   // the short rows' own column slabs (each x slab L2-resident)
         DBuf<int32_t> cnt((size_t)nslab * rows);
         const int g = (int)std::min<int64_t>(((int64_t)rows + 255) / 256, 8192);
-        k_short_count<<<g, 256>>>(rows, nslab, long_min, d_p, d_col, cnt.p);
+        k_short_count<<<g, 256>>>(rows, nslab, long_min, d_p, d_col, cnt.p, sw);
         CPD_CUDA(cudaGetLastError());
         // sp[s][r] = exclusive prefix over (s, r) in slab-major order; sp[s][rows] = end of slab s
         plan.short_ptr.alloc((size_t)nslab * (rows + 1));
@@ -261,7 +266,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
         plan.short_col.alloc(std::max<int64_t>(total, 1));
         plan.short_val.alloc(std::max<int64_t>(total, 1));
         k_short_fill<<<g, 256>>>(rows, nslab, long_min, d_p, d_col, d_val, plan.short_ptr.p, plan.short_col.p,
-                                 plan.short_val.p);
+                                 plan.short_val.p, sw);
         CPD_CUDA(cudaGetLastError());
         CPD_CUDA(cudaDeviceSynchronize());
         plan.short_nnz = total;
@@ -632,8 +637,9 @@ void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc)
     for (Matrix* M : {&P->A, &P->AT})
         if (M->plan.short_on) {
             const int g = (int)std::min<int64_t>(((int64_t)M->rows + 255) / 256, 8192);
-            k_short_fill<<<g, 256>>>(M->rows, M->plan.nslab, WLONG, M->p.p, M->j.p, M->x.p, M->plan.short_ptr.p,
-                                     M->plan.short_col.p, M->plan.short_val.p);
+            k_short_fill<<<g, 256>>>(M->rows, M->plan.short_nslab, WLONG, M->p.p, M->j.p, M->x.p,
+                                     M->plan.short_ptr.p, M->plan.short_col.p, M->plan.short_val.p,
+                                     M->plan.short_width);
         }
     CPD_CUDA(cudaGetLastError());
     CPD_CUDA(cudaDeviceSynchronize());

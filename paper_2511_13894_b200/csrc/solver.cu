@@ -166,7 +166,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         Gate gs = g;
         auto launch_dense = [&]() {
             if (dp.nheavy > 0) {   // heavy rows by dense column blocks (their slots, then k_finish)
-                const size_t DSM = (size_t)NV * (HB + dp.dense_maxitems) * sizeof(double);
+                const size_t DSM = (size_t)NV * HB * sizeof(double);
                 static int dgrid = 0, dsms = 0;
                 static size_t dsm_set = 0;
                 {
@@ -201,10 +201,10 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         };
         if (M.plan.short_on) {
             launch_dense();
-            // per slab: the short rows' slab pass, then the slab's long pieces
-            const int nsl = M.plan.nslab;
+            // the short rows by their own column slabs, then every long piece
+            const int nsl = M.plan.short_nslab;
             for (int sl = 0; sl < nsl; ++sl) {
-                const int grs = std::max(1, std::min<int>(cx.P->num_sms * 8, (M.rows + 255) / 256));
+                const int grs = std::max(1, std::min<int>(cx.P->num_sms * 16, (M.rows + 255) / 256));
                 const bool lastp = sl == nsl - 1;
                 k_short<NV, Epi><<<grs, 256, 0, cx.st>>>(M.dev(), dp, sl, nsl, v0, v1, epi, gs, cx.ctl, cx.bpart.p,
                                                          cx.ctr.p, red, prev, (lastp && single) ? 1 : 0);
@@ -212,9 +212,8 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
                 ++cx.launches;
                 gs.active = nullptr;
                 if (lastp) prev += grs;
-                if (!single && (size_t)sl + 2 < seg.size() && seg[sl + 2] > seg[sl + 1])
-                    launch_items(seg[sl + 1], seg[sl + 2], 0);
             }
+            if (!single && seg.back() > seg[1]) launch_items(seg[1], seg.back(), 0);
         } else {
             // rows items first (x+ just written by the primal step is still in L2), then
             // the heavy rows' dense blocks, then each slab's long pieces
