@@ -225,6 +225,7 @@ cpd_problem* cpd_problem_create_dist_impl(int32_t rank, int32_t world, const cha
         P->world = world;
         P->rank = rank;
         P->split = split;
+        P->push_on = false;   // the short-row push is a single-GPU path
         P->m_glob = m;
         P->n_glob = n;
         P->L = L;

@@ -137,6 +137,9 @@ struct cpd_problem {
     int64_t L = 0;                   // slice length of the split side
     std::vector<int64_t> rank_gofs[2], rank_len[2];   // every rank's owned part (global)
     void* comm = nullptr;            // ncclComm_t (split >= 0)
+    // ---- short-row push: SELL(A^T) entries of short rows flagged
+    bool push_on = false;
+    int64_t push_nnz = 0;
     // ---- row senses (cpd_problem_set_senses; NEXT-2): local rows of A, null = all '='
     cpd::DBuf<int8_t> sense;
     bool has_sense = false;
@@ -190,6 +193,7 @@ struct Ctx {
     DBuf<unsigned> ctr;
     DBuf<double> lpartA, lpartAT;     // long-row piece partials of each layout
     DBuf<double> shortA, shortAT;     // running row sums of the short-row slab passes
+    double* push_acc = nullptr;       // set around the primal/dual pair of a batch (short-row push)
     DBuf<double> red;                 // this rank's totals of the last reduction (distributed)
     DBuf<double> part, recv;          // reduce-scatter send [world][2][L] / receive [2][L] buffers
     int grid_elem = 0;
@@ -230,6 +234,8 @@ void launch_elem(Ctx& cx, int64_t N, const Op& op, Gate g, double* red = nullptr
 
 // diagonal preconditioning of a problem (problem.cu)
 void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc);
+// flag the short-row entries of SELL(A^T) for the push (problem.cu)
+void mark_push(cpd_problem* P);
 
 // distributed problem plumbing (dist.cu)
 void dist_destroy(cpd_problem* P);

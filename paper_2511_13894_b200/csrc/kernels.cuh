@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <type_traits>
 
 namespace cpd {
 
@@ -72,6 +73,7 @@ struct DevPlan {
     const int32_t* short_col;
     const double* short_val;
     double* short_part;           // [NV][rows] running sums across slab passes
+    double* push_acc;             // short-row sums pushed by the primal step (k_csrw rows items read + zero)
     const int32_t* long_row;   // [nlong] row index of each long row
     const int32_t* long_ptr;   // [nlong + 1] piece slots of each long row (column order)
     const int32_t* long_ents;  // k_finish order: nfin_heavy rows (a CTA each), then the rest (a warp each)
@@ -826,11 +828,23 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
 // the gathered vector goes through L1 (no shared memory is used, so L1 keeps its
 // full capacity for the reused entries), and the fused epilogue gets the row sum
 // in the lane that owns the row.  Sum order = CSR order (k ascending).
+// Short-row push: an A^T entry whose row of A is short carries
+// PUSH_BIT in its SELL column index; after the primal epilogue of column j the
+// warp adds a_ij x+_j to acc[i] (fp64 atomics, L2-resident m-vector), and the dual
+// step takes those rows' sums from acc instead of gathering x+ again.
+constexpr int32_t PUSH_BIT = 1 << 30;
+constexpr int32_t COL_MASK = PUSH_BIT - 1;
+template <class E, class = void>
+struct PushRole { static constexpr int v = 0; };   // 1: produces acc (primal step), 2: consumes it (dual step)
+template <class E>
+struct PushRole<E, std::void_t<decltype(E::PUSH)>> { static constexpr int v = E::PUSH; };
+
 struct DevSell {
     const int64_t* __restrict__ sp;
     const int32_t* __restrict__ col;
     const double* __restrict__ val;
     int32_t rows, nslice;
+    double* push = nullptr;   // acc (m) when this pass pushes its short-row products
 };
 
 constexpr int TPB_SELL = 256;
@@ -872,6 +886,8 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
     const int lane = threadIdx.x & 31;
     const int nw = gridDim.x * (TPB_SELL / 32);
     __shared__ double vst[TPB_SELL / 32][(NVEC > 0 ? NVEC : 1) * 32];
+    // push only for an iteration the dual step will complete (k < k_stop)
+    const bool push_on = M.push != nullptr && ctl->k < ctl->k_stop;
     for (int s = (blockIdx.x * TPB_SELL + threadIdx.x) >> 5; s < M.nslice; s += nw) {
         const int64_t b = M.sp[s];
         const int len = (int)((M.sp[s + 1] - b) >> 5);
@@ -909,8 +925,8 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
             double g[SELL_U], g2[SELL_U];
 #pragma unroll
             for (int u = 0; u < SELL_U; ++u) {
-                g[u] = c[u] >= 0 ? __ldg(&v0[c[u]]) : 0.0;
-                if (NV > 1) g2[u] = c[u] >= 0 ? __ldg(&v1[c[u]]) : 0.0;
+                g[u] = c[u] >= 0 ? __ldg(&v0[c[u] & COL_MASK]) : 0.0;
+                if (NV > 1) g2[u] = c[u] >= 0 ? __ldg(&v1[c[u] & COL_MASK]) : 0.0;
             }
             int cn[SELL_U];
             double an[SELL_U];
@@ -935,6 +951,15 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
                 vs[v] = stg + v * 32;
             }
             e.row(r, sm, vs, lane, acc);
+            if constexpr (PushRole<Epi>::v == 1) {
+                if (push_on) {   // a_ij x+_j into acc[i] for the short rows i of column j
+                    const double xp = e.pushval(r);
+                    for (int k = 0; k < len; ++k) {
+                        const int32_t cc = cp[(int64_t)k * 32];
+                        if (cc >= 0 && (cc & PUSH_BIT)) atomicAdd(&M.push[cc & COL_MASK], vp[(int64_t)k * 32] * xp);
+                    }
+                }
+            }
         }
     }
     grid_finalize<NS, TPB_SELL>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
@@ -1013,6 +1038,12 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
             double racc[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) racc[v] = 0.0;
+            if (PushRole<Epi>::v == 2 && P.push_acc) {   // sums pushed by the primal step
+                if (lane < nr) {
+                    racc[0] = P.push_acc[r0 + lane];
+                    P.push_acc[r0 + lane] = 0.0;
+                }
+            } else {
             // two-stage software pipeline: the next round's indices / values are in
             // flight while this round's gathers are
             int c[WU];
@@ -1068,6 +1099,7 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
                     c[u] = cn[u];
                     a[u] = an[u];
                 }
+            }
             }
             if (lane < nr) {
                 const double* vs[NVEC > 0 ? NVEC : 1];
@@ -1362,6 +1394,8 @@ template <bool PE>
 struct EpiPrimalT {
     static constexpr int NS = 4;   // c^T x_k, ||r_D(y_k)||^2, bound terms, #nonfinite(x_{k+1})
     static constexpr int NVEC = PE ? 5 : 3;
+    static constexpr int PUSH = 1;
+    __device__ __forceinline__ double pushval(int j) const { return xn[j]; }
     const double* c;
     Bounds bd;
     PingPong X, Xa;
@@ -1434,6 +1468,7 @@ using EpiPrimal = EpiPrimalT<true>;
 struct EpiDual {
     static constexpr int NS = 3;   // ||b - A x_{k+1}||^2, b^T y_{k+1}, #nonfinite(y_{k+1})
     static constexpr int NVEC = 4;
+    static constexpr int PUSH = 2;
     const double* b;
     double *y, *ya, *ax;
     double sigma, inv_t;

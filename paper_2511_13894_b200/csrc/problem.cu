@@ -322,6 +322,36 @@ __global__ void k_sell_fill(int32_t rows, int32_t nslice, const int32_t* p, cons
     }
 }
 
+// Mark the SELL entries of A^T whose row of A is short (<= WLONG entries: the warp
+// plan's rows items) with PUSH_BIT (short-row push).
+__global__ void k_mark_push(int64_t N, int32_t* scol, const int32_t* Ap)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = scol[q];
+        if (c >= 0 && Ap[c + 1] - Ap[c] <= WLONG) scol[q] = c | PUSH_BIT;
+    }
+}
+
+void mark_push(cpd_problem* P)
+{
+    P->push_on = false;
+    const char* pe = getenv("CPD_PUSH");
+    if (pe && pe[0] == '0') return;
+    if (P->split >= 0 || !P->AT.sell.on || !P->A.plan.warp || P->m >= PUSH_BIT) return;
+    const int64_t N = P->AT.sell.padded;
+    k_mark_push<<<(int)std::min<int64_t>((N + 255) / 256, 65536), 256>>>(N, P->AT.sell.col.p, P->A.p.p);
+    CPD_CUDA(cudaGetLastError());
+    CPD_CUDA(cudaDeviceSynchronize());
+    // short-row nonzeros (their K2 reads move to K1's push)
+    std::vector<int32_t> hp((size_t)P->m + 1);
+    CPD_CUDA(cudaMemcpy(hp.data(), P->A.p.p, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
+    int64_t sn = 0;
+    for (int32_t i = 0; i < P->m; ++i)
+        if (hp[i + 1] - hp[i] <= WLONG) sn += hp[i + 1] - hp[i];
+    P->push_nnz = sn;
+    P->push_on = true;
+}
+
 void build_sell(Matrix& M, int64_t nnz, double max_ratio)
 {
     Sell& S = M.sell;
@@ -634,6 +664,7 @@ void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc)
     // derived copies of the values
     if (P->AT.sell.on) build_sell(P->AT, P->nnz, 1.25);
     if (P->A.sell.on) build_sell(P->A, P->nnz, 1.25);
+    if (P->push_on) mark_push(P);
     for (Matrix* M : {&P->A, &P->AT})
         if (M->plan.short_on) {
             const int g = (int)std::min<int64_t>(((int64_t)M->rows + 255) / 256, 8192);
@@ -770,6 +801,7 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         // (A^T only: for A the dual epilogue's four staged vectors favour the TMA plan
         // kernel, measured on C4 — profiles/r01_kernel_iterations.md)
         if (sell_ok && nnz <= (int64_t)n * 64) build_sell(P->AT, nnz, 1.25);
+        mark_push(P);
         CPD_CUDA(cudaDeviceSynchronize());
     } catch (...) {
         delete P;

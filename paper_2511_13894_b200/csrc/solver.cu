@@ -75,7 +75,8 @@ DevPlan Ctx::planA() const
 {
     const Plan& pl = P->A.plan;
     return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
-                   pl.dense_ptr.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortA.p, pl.long_row.p,
+                   pl.dense_ptr.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortA.p, nullptr,
+                   pl.long_row.p,
                    pl.long_ptr.p, pl.long_ents.p, pl.nfin_heavy, lpartA.p};
 }
 
@@ -83,7 +84,8 @@ DevPlan Ctx::planAT() const
 {
     const Plan& pl = P->AT.plan;
     return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
-                   pl.dense_ptr.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortAT.p, pl.long_row.p,
+                   pl.dense_ptr.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortAT.p, nullptr,
+                   pl.long_row.p,
                    pl.long_ptr.p, pl.long_ents.p, pl.nfin_heavy, lpartAT.p};
 }
 
@@ -140,7 +142,9 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
             }
         }
         const int gr = std::max(1, std::min<int>(sgrid, (M.sell.nslice + 7) / 8));
-        k_sell<NV, Epi><<<gr, TPB_SELL, 0, cx.st>>>(M.dsell(), v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p, red);
+        DevSell ds = M.dsell();
+        if (PushRole<Epi>::v == 1) ds.push = cx.push_acc;
+        k_sell<NV, Epi><<<gr, TPB_SELL, 0, cx.st>>>(ds, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p, red);
         CPD_CUDA(cudaGetLastError());
         ++cx.launches;
         return;
@@ -189,6 +193,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         };
         auto launch_items = [&](int a, int b, int fin) {
             DevPlan ds = dp;
+            if (PushRole<Epi>::v == 2) ds.push_acc = cx.push_acc;
             ds.ent = dp.ent + a;
             ds.nent = b - a;
             const int gr = std::max(1, std::min<int>(wgrid, (ds.nent + 7) / 8));
@@ -553,6 +558,7 @@ struct cpd_solver {
     DBuf<double> X0, X1, Xa0, Xa1, Xr, Y, Ya, Yr, AX, AXa, Ystar, Z, lhat, uhat, chat, objd, SN, SM;
     DBuf<double> LHo, UHo, TX, TY;   // scaled problems: original-space model bounds; unscale scratch
     DBuf<int8_t> shat;                // corner-model row senses
+    DBuf<double> ACC;                 // short-row push sums (m), zero between iterations
     int64_t rows_eq = 0;
     // replicas of the split side (world * L): current vector / its average
     DBuf<double> RV, RA;
@@ -586,6 +592,10 @@ struct cpd_solver {
         for (auto* b : {&Y, &Ya, &Yr, &AX, &AXa, &Ystar, &SM}) b->alloc(m);
         for (auto* b : {&X0, &X1, &Xa0, &Xa1, &Xr, &Z}) CPD_CUDA(cudaMemset(b->p, 0, sizeof(double) * n));
         for (auto* b : {&Y, &Ya, &Yr, &AX, &AXa, &Ystar}) CPD_CUDA(cudaMemset(b->p, 0, sizeof(double) * m));
+        if (p->push_on) {
+            ACC.alloc(std::max<int32_t>(p->m, 1));
+            CPD_CUDA(cudaMemset(ACC.p, 0, sizeof(double) * p->m));
+        }
         if (p->split >= 0) {
             const size_t R = (size_t)p->world * p->L;
             RV.alloc(R);
@@ -661,6 +671,7 @@ struct cpd_solver {
         h.traj_off = troff.p;
         h.traj_rp = trrp.p;
         cx.push_ctl(h);
+        if (ACC.p) CPD_CUDA(cudaMemsetAsync(ACC.p, 0, sizeof(double) * P->m, cx.st));   // no stale pushes
         Reps rp(P, RV.p);
         if (rc.power) power_iterate(cx, rp, prm.power_iters, prm.seed, SN.p, SM.p);   // writes ctl->eta
         const double* c = obj_of(rc.kind);
@@ -734,6 +745,7 @@ struct cpd_solver {
             refresh(cx, 0, fixed(Y.p), RV.p, gr);   // y may have changed
             rec(ev1, NODE_RESTART);
         }
+        cx.push_acc = ACC.p;   // primal step pushes short-row products, dual step consumes them
         for (int s = 0; s < K; ++s) {
             const int n1 = NODE_K0 + 2 * s, n2 = n1 + 1;
             const Gate g1{GATE_K1, s, n1, active.p}, g2{GATE_K2, s, n2, active.p};
@@ -761,6 +773,7 @@ struct cpd_solver {
             refresh(cx, 0, fixed(Y.p), RV.p, always());
             rec(ev1, n2);
         }
+        cx.push_acc = nullptr;
         if (capture) graph_kernels[kind] = cx.launches - l0;
         CPD_CUDA(cudaMemcpyAsync(h_active, active.p, sizeof(int32_t) * nnodes, cudaMemcpyDeviceToHost, cx.st));
         CPD_CUDA(cudaMemcpyAsync(cx.h_ctl, cx.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, cx.st));
@@ -1099,8 +1112,12 @@ struct cpd_solver {
         const bool corner = name.find(":corner") != std::string::npos;
         const std::string base = name.substr(0, name.find(':'));
         const double bnd = (corner || !P->uniform_bounds) ? 16.0 * n : 0.0;
-        if (base == "primal_step_AT") return 12 * nnz + 4 * (nr + 1) + 8 * mr + 40 * n + bnd;
-        if (base == "dual_step_A") return 12 * nnz + 4 * (mr + 1) + 8 * nr + 56 * m;
+        // short-row push: their entries are read again by K1 (12 B) and not by K2; K2
+        // reads and zeroes acc (16 B per row)
+        const double pz = P->push_on ? (double)P->push_nnz : 0.0;
+        if (base == "primal_step_AT") return 12 * nnz + 4 * (nr + 1) + 8 * mr + 40 * n + bnd + 12 * pz;
+        if (base == "dual_step_A")
+            return 12 * (nnz - pz) + 4 * (mr + 1) + 8 * nr + 56 * m + (P->push_on ? 16.0 * mr : 0.0);
         if (base == "check_eval_AT")
             return 12 * nnz + 4 * (nr + 1) + (prm.restart ? 16 : 8) * mr + 32 * n + bnd + (corner ? 16 * n : 0);
         if (base == "check_eval_A") return 12 * nnz + 4 * (mr + 1) + 8 * nr + 40 * m;

@@ -300,3 +300,33 @@ def test_every_spmv_format_lockstep(name, fmt, monkeypatch):
     xo, yo = R.get()
     assert close(xg, xo) and close(yg, yo), (name, fmt)
     assert P.power_sigma(128, 7) == pytest.approx(oracle.power_sigma(olp, 128, 7), rel=1e-12)
+
+
+@pytest.mark.parametrize("push", ["1", "0"])
+@pytest.mark.parametrize("name", ["c5-s", "c2-s"])
+def test_short_row_push_lockstep(name, push, monkeypatch):
+    """The short-row push (primal step scatters a_ij x+_j into an L2-resident m-vector
+    with fp64 atomics; the dual step reads it instead of gathering x+) meets the same
+    1e-9 contract as the pull path; with CPD_WARP=1 so that C2's A takes the
+    warp plan too."""
+    monkeypatch.setenv("CPD_PUSH", push)
+    monkeypatch.setenv("CPD_WARP", "1")
+    lp = lpgen.config(name)
+    olp = oracle.OracleLP(lp)
+    P = cpd.Problem.from_lp(lp)
+    eta = 0.9 / oracle.power_sigma(olp)
+    S = cpd.Solver(P, step_size=eta, restart=1)
+    R = oracle.Run(olp, oracle.default_params(step_size=eta, restart=1), mode=oracle.MODE_NONE)
+    for k in (64, 300, 1000):
+        S.step(k - R.k)
+        R.run(k - R.k)
+        xg, yg = S.get_iterate()
+        xo, yo = R.get()
+        assert close(xg, xo) and close(yg, yo), (name, push, k)
+    # termination and corner phase through the push path
+    S2 = cpd.Solver(P)
+    r = S2.solve()
+    xo, yo, ro = oracle.solve(olp, oracle.default_params())
+    assert r["status"] == ro["status"] == 0
+    assert abs(r["iterations"] - ro["iterations"]) <= max(1, 0.01 * ro["iterations"])
+    assert r["pobj"] == pytest.approx(ro["pobj"], rel=1e-6)
