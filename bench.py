@@ -372,7 +372,6 @@ def e2e_measure(args, lp, dev, rank=0, world=1):
     d2h = xo.nbytes + yo.nbytes + zo.nbytes
     steps = args.e2e_steps or max(1, min(args.steps, 2))
 
-    uid = None
     if world > 1:
         import torch.distributed as dist
 

@@ -121,8 +121,6 @@ static std::vector<int64_t> balanced_blocks(const std::vector<int64_t>& len, int
 
 using namespace cpd;
 
-static thread_local std::string g_derr;
-
 extern "C" {
 
 /* see include/cpd.h */
@@ -229,7 +227,6 @@ cpd_problem* cpd_problem_create_dist_impl(int32_t rank, int32_t world, const cha
         P->m_glob = m;
         P->n_glob = n;
         P->L = L;
-        const int local = 1 - split;   // the side with nnz-balanced blocks
         for (int s = 0; s < 2; ++s) {
             P->rank_gofs[s].assign(world, 0);
             P->rank_len[s].assign(world, 0);
@@ -247,7 +244,6 @@ cpd_problem* cpd_problem_create_dist_impl(int32_t rank, int32_t world, const cha
             P->gofs[s] = P->rank_gofs[s][rank];
             P->poff[s] = (s == split) ? P->gofs[s] : 0;   // the local problem holds all rows of the split side
         }
-        (void)local;
 #ifdef CPD_HAVE_NCCL
         ncclUniqueId u;
         std::memcpy(&u, id, 128);

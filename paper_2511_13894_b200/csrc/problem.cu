@@ -89,7 +89,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     plan.warp = warp ? 1 : 0;
     std::vector<PlanEntry> ent;
     std::vector<int32_t> lrows;
-    int64_t nrows_e = 0, nsingle = 0;
+    int64_t nrows_e = 0;
     int32_t r0 = 0;
     int64_t cur = 0;
     auto flush = [&](int32_t r1) {
@@ -208,7 +208,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
         CPD_CUDA(cudaMemcpy(plan.dense_ent.p, dent.data(), sizeof(PlanEntry) * dent.size(), cudaMemcpyHostToDevice));
         CPD_CUDA(cudaMemcpy(plan.dense_ptr.p, dptr.data(), sizeof(int32_t) * (nhb + 1), cudaMemcpyHostToDevice));
     }
-    std::vector<int32_t> next(lptr.begin(), lptr.end() - 1), lents;
+    std::vector<int32_t> next(lptr.begin(), lptr.end() - 1);
     int64_t npieces = 0;
     plan.seg.assign(1, 0);
     plan.seg.push_back((int32_t)ent.size());
@@ -224,9 +224,8 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     plan.nent = (int32_t)ent.size();
     plan.nlong = nl;
     plan.rows_entries = nrows_e;
-    plan.single_entries = nsingle;
+    plan.single_entries = 0;
     plan.long_pieces = (int64_t)lptr[nl];
-    (void)lents;
     plan.nslab = nslab;
     // warp plan with >= 2 slabs: short rows also by slab (k_short), so their gathers of
     // the vector hit the L2-resident slab instead of DRAM
