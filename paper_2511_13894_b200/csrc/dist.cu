@@ -20,7 +20,9 @@
 
 #ifdef CPD_HAVE_NCCL
 #include <nccl.h>
+#include <nccl_device.h>
 #endif
+#include <cstdlib>
 
 cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const int32_t* Ap,
                                      const int32_t* Aj, const double* Ax, const int32_t* ATp,
@@ -45,6 +47,46 @@ void dist_destroy(cpd_problem* P)
     if (P->comm) ncclCommDestroy((ncclComm_t)P->comm);
 #endif
     P->comm = nullptr;
+}
+
+#ifdef CPD_HAVE_NCCL
+// base of every rank's receive window (NCCL symmetric memory, LSA over NVLink)
+__global__ void k_peer_bases(ncclWindow_t w, int world, double** out)
+{
+    for (int q = threadIdx.x; q < world; q += blockDim.x) out[q] = (double*)ncclGetPeerPointer(w, 0, q);
+}
+#endif
+
+void Ctx::p2p_setup()
+{
+    const char* e = getenv("CPD_P2P");
+    if (P->split < 0 || !(e && e[0] == '1')) return;
+#ifdef CPD_HAVE_NCCL
+    const size_t bytes = ((size_t)P->world * 2 * P->L * sizeof(double) + 4095) & ~(size_t)4095;
+    void* buf = nullptr;
+    CPD_NCCL(ncclMemAlloc(&buf, bytes));
+    winbuf = (double*)buf;
+    CPD_CUDA(cudaMemset(winbuf, 0, bytes));
+    ncclWindow_t w;
+    CPD_NCCL(ncclCommWindowRegister(comm_of(P), buf, bytes, &w, NCCL_WIN_COLL_SYMMETRIC));
+    win = w;
+    peer.alloc(P->world);
+    k_peer_bases<<<1, 32, 0, st>>>(w, P->world, peer.p);
+    CPD_CUDA(cudaGetLastError());
+    CPD_CUDA(cudaStreamSynchronize(st));
+    p2p = true;
+#endif
+}
+
+void Ctx::p2p_teardown()
+{
+#ifdef CPD_HAVE_NCCL
+    if (win) ncclCommWindowDeregister(comm_of(P), (ncclWindow_t)win);
+    if (winbuf) ncclMemFree(winbuf);
+#endif
+    win = nullptr;
+    winbuf = nullptr;
+    p2p = false;
 }
 
 void Ctx::allreduce_sum(double* buf, int64_t count)

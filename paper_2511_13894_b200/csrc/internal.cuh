@@ -196,6 +196,14 @@ struct Ctx {
     double* push_acc = nullptr;       // set around the primal/dual pair of a batch (short-row push)
     DBuf<double> red;                 // this rank's totals of the last reduction (distributed)
     DBuf<double> part, recv;          // reduce-scatter send [world][2][L] / receive [2][L] buffers
+    // fused split product (CPD_P2P=1): symmetric receive window [world][2][L] and the
+    // device table of every rank's window base
+    bool p2p = false;
+    void* win = nullptr;              // ncclWindow_t
+    double* winbuf = nullptr;         // ncclMemAlloc'ed
+    DBuf<double*> peer;
+    void p2p_setup();
+    void p2p_teardown();
     int grid_elem = 0;
     int64_t launches = 0;            // kernels of this library launched on `st` (graph nodes included)
     explicit Ctx(const cpd_problem* p);

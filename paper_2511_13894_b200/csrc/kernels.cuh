@@ -1368,6 +1368,61 @@ struct EpiStore {
     __device__ void finalize(const double*, Ctl*) const {}
 };
 
+// Fused split product (CPD_P2P=1): row r's NV sums are stored straight into the
+// owner rank's receive window over NVLink peer memory (NCCL symmetric window),
+// slot [this rank][v][r - q L], while the SpMV streams; after a barrier the owner
+// sums the world slots of each owned row in rank order (k_slice_p2p).
+template <int NV_>
+struct EpiStorePeer {
+    static constexpr int NS = 1;
+    static constexpr int NVEC = 0;
+    double* const* peer;   // [world] base of every rank's receive window (device pointers)
+    int64_t L;
+    int32_t rank;
+    __device__ void load(const Ctl*) {}
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
+    __device__ __forceinline__ void row(int r, const double* s, const double* const*, int, double*) const
+    {
+        const int64_t q = r / L;
+        double* d = peer[q] + ((int64_t)rank * NV_) * L + (r - q * L);
+#pragma unroll
+        for (int v = 0; v < NV_; ++v) d[v * L] = s[v];
+    }
+    __device__ void finalize(const double*, Ctl*) const {}
+};
+
+// Owned-slice epilogue of a fused split product: sum of the world ranks' slots.
+template <int NV, class Epi>
+__global__ void __launch_bounds__(TPB)
+k_slice_p2p(int64_t N, int64_t L, int32_t world, const double* __restrict__ win, Epi epi, Gate gate, Ctl* ctl,
+            double* bpart, unsigned* ctr, double* red)
+{
+    constexpr int NS = Epi::NS;
+    constexpr int NVEC = Epi::NVEC;
+    __shared__ int s_go;
+    if (threadIdx.x == 0) s_go = gate_open(gate, ctl);
+    __syncthreads();
+    if (!s_go) return;
+    Epi e = epi;
+    e.load(ctl);
+    const double* vin[NVEC > 0 ? NVEC : 1];
+#pragma unroll
+    for (int v = 0; v < NVEC; ++v) vin[v] = e.vec(v);
+    double acc[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < N; i += (int64_t)gridDim.x * TPB) {
+        double sm[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sm[v] = 0.0;
+        for (int p = 0; p < world; ++p)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) sm[v] += win[((int64_t)p * NV + v) * L + i];
+        e.row((int)i, sm, vin, (int)i, acc);
+    }
+    grid_finalize<NS>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+}
+
 // Replica refresh: dst[i] = src(k)[i] for i < N (the owned slice, copied into its
 // place in the all-gather buffer).
 static __global__ void __launch_bounds__(TPB) k_copy_sel(int64_t N, double* dst, VecSel src, Gate gate, Ctl* ctl)

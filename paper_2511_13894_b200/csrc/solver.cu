@@ -62,10 +62,12 @@ Ctx::Ctx(const cpd_problem* p) : P(p)
         CPD_CUDA(cudaMemset(recv.p, 0, sizeof(double) * 2 * p->L));
     }
     grid_elem = p->num_sms * 4;
+    p2p_setup();
 }
 
 Ctx::~Ctx()
 {
+    p2p_teardown();
     if (h_main) cudaFreeHost(h_main);
     if (h_aux) cudaFreeHost(h_aux);
     if (st) cudaStreamDestroy(st);
@@ -305,7 +307,21 @@ static void pass(Ctx& cx, int side, VecSel v0, VecSel v1, const Epi& epi, Gate g
         launch_spmv<NV>(cx, M, dp, v0, v1, epi, g, nullptr);
         return;
     }
-    if (P->split == side) {
+    if (P->split == side && cx.p2p) {
+        // fused: the SpMV stores each row sum into its owner's window (NVLink peer
+        // memory); a one-scalar allreduce is the barrier before the owners' sums
+        EpiStorePeer<NV> es{cx.peer.p, P->L, P->rank};
+        launch_spmv<NV>(cx, M, dp, v0, v1, es, g, nullptr);
+        cx.allreduce_sum(cx.red.p + NSMAX - 1, 1);
+        const int64_t N = P->own_len[side];
+        const int gr = (int)std::max<int64_t>(1, std::min<int64_t>((N + TPB - 1) / TPB, cx.grid_elem));
+        Gate g2 = g;
+        g2.active = nullptr;
+        k_slice_p2p<NV, Epi><<<gr, TPB, 0, cx.st>>>(N, P->L, P->world, cx.winbuf, epi, g2, cx.ctl, cx.bpart.p,
+                                                    cx.ctr.p, cx.red.p);
+        CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
+    } else if (P->split == side) {
         EpiStore<NV> es{cx.part.p, P->L};
         launch_spmv<NV>(cx, M, dp, v0, v1, es, g, nullptr);
         cx.reduce_scatter(cx.part.p, cx.recv.p, (int64_t)NV * P->L);

@@ -114,3 +114,30 @@ def test_dist_solve_and_corner(dist_problems, name, part):
     ref = oracle.stats(lp.m, xg, zg, lp.lb, lp.ub, model["lhat"], model["uhat"], 1e-6, 100)
     for k in ("off_bound", "off_bound_strict", "off_bound_model", "zero_rc", "candidates"):
         assert after[k] == ref[k], k
+
+
+@pytest.mark.parametrize("part", [0, 1])
+@pytest.mark.parametrize("name", ["c2-s", "c5-s"])
+def test_fused_p2p_split_path(name, part, monkeypatch):
+    """CPD_P2P=1: the split product stores its row sums straight into the owner's
+    NCCL symmetric window (peer memory) instead of a separate reduce-scatter; with
+    one rank the peer is this GPU.  Same 1e-9 iterate contract and termination."""
+    monkeypatch.setenv("CPD_P2P", "1")
+    lp = lpgen.config(name)
+    olp = oracle.OracleLP(lp)
+    P = cpd.Problem.create_dist(lp, 0, 1, cpd.nccl_unique_id(), partition=part, device=0)
+    eta = 0.9 / oracle.power_sigma(olp)
+    S = cpd.Solver(P, step_size=eta, restart=1)
+    R = oracle.Run(olp, oracle.default_params(step_size=eta, restart=1), mode=oracle.MODE_NONE)
+    for k in (1, 65, 1000):
+        S.step(k - R.k)
+        R.run(k - R.k)
+        xg, yg = S.get_iterate()
+        xo, yo = R.get()
+        assert close(xg, xo) and close(yg, yo), (name, part, k)
+    S2 = cpd.Solver(P, max_iters=3000)
+    r = S2.solve()
+    xo, yo, ro = oracle.solve(olp, oracle.default_params(max_iters=3000))
+    assert r["status"] == ro["status"]
+    assert abs(r["iterations"] - ro["iterations"]) <= max(1, 0.01 * ro["iterations"])
+    assert r["pobj"] == pytest.approx(ro["pobj"], rel=1e-6)
