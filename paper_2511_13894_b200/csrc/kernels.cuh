@@ -207,6 +207,32 @@ __device__ __forceinline__ double ld_keep(const double* p)
 #endif
 }
 
+// Streamed (read-once) loads of matrix indices / values: evict-first in L1 and L2
+// (ld.global.cs), or with CPD_NOALLOC=1 not allocated in L1 at all.
+#ifndef CPD_NOALLOC
+#define CPD_NOALLOC 0
+#endif
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p)
+{
+#if CPD_NOALLOC
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#else
+    return __ldcs(p);
+#endif
+}
+__device__ __forceinline__ double ld_stream(const double* p)
+{
+#if CPD_NOALLOC
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#else
+    return __ldcs(p);
+#endif
+}
+
 // KKT score terms (S-3): o = {rp, rd, pobj, dobj, r_p, r_d, r_g, score}
 __device__ __forceinline__ void score8(double rp2, double rd2, double pobj, double dobj,
                                        double nb, double nc, double* o)
@@ -914,8 +940,8 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
 #pragma unroll
             for (int u = 0; u < SELL_U; ++u) {
                 const bool ok = k0 + u < len;
-                cc[u] = ok ? __ldcs(cp + (int64_t)(k0 + u) * 32) : -1;
-                aa[u] = ok ? __ldcs(vp + (int64_t)(k0 + u) * 32) : 0.0;
+                cc[u] = ok ? ld_stream(cp + (int64_t)(k0 + u) * 32) : -1;
+                aa[u] = ok ? ld_stream(vp + (int64_t)(k0 + u) * 32) : 0.0;
             }
         };
         int c[SELL_U];
@@ -1017,8 +1043,8 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
 #pragma unroll
             for (int u = 0; u < WU; ++u) {
                 const int q = base + 32 * u + lane;
-                cc[u] = q < T ? __ldcs(M.j + p0 + q) : -1;
-                aa[u] = q < T ? __ldcs(M.x + p0 + q) : 0.0;
+                cc[u] = q < T ? ld_stream(M.j + p0 + q) : -1;
+                aa[u] = q < T ? ld_stream(M.x + p0 + q) : 0.0;
             }
         };
         if (E.b >= 0) {
@@ -1200,8 +1226,8 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
 #pragma unroll
                 for (int u = 0; u < DU; ++u) {
                     const int qq = q + 32 * u;
-                    c[u] = qq < E.p1 ? __ldcs(M.j + qq) - j0 : -1;
-                    a[u] = qq < E.p1 ? __ldcs(M.x + qq) : 0.0;
+                    c[u] = qq < E.p1 ? ld_stream(M.j + qq) - j0 : -1;
+                    a[u] = qq < E.p1 ? ld_stream(M.x + qq) : 0.0;
                 }
 #pragma unroll
                 for (int u = 0; u < DU; ++u)
