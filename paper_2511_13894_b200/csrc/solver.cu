@@ -16,6 +16,7 @@
 // ranks take identical decisions.  With one GPU (split < 0) pass<> is exactly
 // the single fused kernel with its last-CTA finalize.
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -31,6 +32,11 @@ namespace cpd {
 Ctx::Ctx(const cpd_problem* p) : P(p)
 {
     CPD_CUDA(cudaSetDevice(p->device));
+    // L2 fetch granularity for the random gathers (CPD_L2FETCH=32/64/128 bytes; device-wide)
+    if (const char* lf = getenv("CPD_L2FETCH")) {
+        const int g = atoi(lf);
+        if (g > 0) CPD_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)g));
+    }
     CPD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     ctl_main.alloc(1);
     ctl_aux.alloc(1);
