@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--ref-iters", type=int, default=0, help="oracle iterations per reference step (0: auto)")
     ap.add_argument("--partition", type=int, default=-1,
                     help="multi-GPU partition: 0 row-block, 1 col-block, -1 auto (shard the long side)")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the distributed (split) path even with one rank (checks the N>1 code path)")
     return ap.parse_args()
 
 
@@ -270,13 +272,16 @@ def main():
     dev = local
     torch.cuda.set_device(dev)
     uid = None
+    dist_path = world > 1 or args.force_dist
     if world > 1:
         import torch.distributed as dist
         obj = [cpd.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
+    elif dist_path:
+        uid = cpd.nccl_unique_id()
     # resident problem (a0: validation + transpose + plans happen here, untimed)
-    if world > 1:
+    if dist_path:
         P = cpd.Problem.create_dist(lp, rank, world, uid, partition=args.partition, device=dev)
     else:
         P = cpd.Problem.from_lp(lp, device=dev)
@@ -337,10 +342,10 @@ def main():
     S.close()
     P.close()
     if with_e2e:
-        res["e2e"] = e2e_measure(args, lp, dev, rank, world)
+        res["e2e"] = e2e_measure(args, lp, dev, rank, world, dist_path)
     clk_s = clk.summary()
     res["clocks"] = clk_s
-    if world > 1:
+    if dist_path:
         res["partition"] = {0: "row-block", 1: "col-block"}[P_info["partition"]]
     if args.tte and world == 1:
         try:
@@ -353,7 +358,7 @@ def main():
         print(json.dumps(res), flush=True)
 
 
-def e2e_measure(args, lp, dev, rank=0, world=1):
+def e2e_measure(args, lp, dev, rank=0, world=1, dist_path=False):
     """Public API with HOST buffers: H2D of the LP from pinned memory, problem
     creation (device validation + transpose), solve + corner push, D2H of x, y, z.
     N > 1: every rank creates its block from the same host arrays (collective)."""
@@ -376,9 +381,10 @@ def e2e_measure(args, lp, dev, rank=0, world=1):
         import torch.distributed as dist
 
     def one():
-        if world > 1:
+        if dist_path:
             obj = [cpd.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
+            if world > 1:
+                dist.broadcast_object_list(obj, src=0)
             import types
             hl = types.SimpleNamespace(m=lp.m, n=lp.n, ATp=pin["ATp"], ATj=pin["ATj"], ATx=pin["ATx"], b=pin["b"],
                                        c=pin["c"], lb=pin["lb"], ub=pin["ub"])
