@@ -34,6 +34,10 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# stdout carries exactly one JSON line: NCCL's own log (its version banner included)
+# goes to stderr
+os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 METRIC = "PDHG iterations/sec and achieved HBM GB/s (fp64) at 1/2/4/8 B200; time to eps=1e-4"
 UNIT = "iter/s"
