@@ -34,10 +34,15 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# stdout carries exactly one JSON line: NCCL's own log (its version banner included)
-# goes to stderr
-os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
-os.environ.setdefault("NCCL_DEBUG", "WARN")
+# stdout carries exactly one JSON line: everything else any library prints on file
+# descriptor 1 (NCCL's version banner, ...) is sent to stderr, and the JSON line is
+# written to the saved original stdout
+_JSON_FD = os.dup(1)
+os.dup2(2, 1)
+
+
+def emit(res):
+    os.write(_JSON_FD, (json.dumps(res) + "\n").encode())
 
 METRIC = "PDHG iterations/sec and achieved HBM GB/s (fp64) at 1/2/4/8 B200; time to eps=1e-4"
 UNIT = "iter/s"
@@ -269,7 +274,7 @@ def main():
     if args.impl == "reference":
         res = reference_arm(args, lp, rank, world)
         if rank == 0:
-            print(json.dumps(res), flush=True)
+            emit(res)
         return
     import torch
     import paper_2511_13894_b200 as cpd
@@ -359,7 +364,7 @@ def main():
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         res["cpu_baseline"] = cpu_baseline(lp)
     if rank == 0:
-        print(json.dumps(res), flush=True)
+        emit(res)
 
 
 def e2e_measure(args, lp, dev, rank=0, world=1, dist_path=False):
