@@ -24,7 +24,7 @@ import paper_2511_13894_b200 as cpd  # noqa: E402
 
 
 def run_one(lp, eps_abs=1e-6, obj_scale=1.0, max1=200000, max2=200000, traj=True):
-    P = cpd.Problem.from_lp(lp)
+    P = cpd.Problem.from_lp(lp)   # (row senses of lp, if any, are applied by from_lp)
     S = cpd.Solver(P, max_iters=max1)
     t0 = time.time()
     r1 = S.solve()
@@ -39,6 +39,7 @@ def run_one(lp, eps_abs=1e-6, obj_scale=1.0, max1=200000, max2=200000, traj=True
     # objective of x^ in the ORIGINAL model (how far steering moved the primal objective)
     x, y = S.get_iterate()
     out["corner_pobj_orig"] = float(lp.c @ x)
+    out["rows_eq"] = after.get("rows_eq", 0)
     if traj:
         k, off, rp = S.trajectory()
         out["trajectory"] = {"k": k.tolist(), "off_bound": off.tolist(), "rp": rp.tolist()}
@@ -49,15 +50,17 @@ def run_one(lp, eps_abs=1e-6, obj_scale=1.0, max1=200000, max2=200000, traj=True
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c1,c2,c3-s,c4-s,c2-s")
+    ap.add_argument("--configs", default="c1,c2,c3-s,c4-s,c2-s,c3,c4,c4-ineq")
+    ap.add_argument("--sweep", default="c1,c2,c3-s,c4-s,c2-s", help="configs that also get the obj_scale / eps_abs sweeps")
     ap.add_argument("--out", default="profiles/r01_corner_study")
     a = ap.parse_args()
     res = {}
     for name in a.configs.split(","):
         lp = lpgen.config(name)
-        res[name] = {"base": run_one(lp)}
-        res[name]["obj_scale"] = {str(s): run_one(lp, obj_scale=s, traj=False) for s in (1e-6, 1e-4)}
-        res[name]["eps_abs"] = {str(e): run_one(lp, eps_abs=e, traj=False) for e in (1e-4, 1e-2)}
+        res[name] = {"base": run_one(lp), "obj_scale": {}, "eps_abs": {}}
+        if name in a.sweep.split(","):
+            res[name]["obj_scale"] = {str(s): run_one(lp, obj_scale=s, traj=False) for s in (1e-6, 1e-4)}
+            res[name]["eps_abs"] = {str(e): run_one(lp, eps_abs=e, traj=False) for e in (1e-4, 1e-2)}
         print(name, json.dumps({k: v for k, v in res[name]["base"].items() if k != "trajectory"}), flush=True)
     with open(a.out + ".json", "w") as f:
         json.dump(res, f, indent=1)
