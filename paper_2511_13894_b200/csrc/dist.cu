@@ -234,6 +234,10 @@ cpd_problem* cpd_problem_create_dist_impl(int32_t rank, int32_t world, const cha
     const int64_t b0 = bnd[rank], b1 = bnd[rank + 1];
 
     cpd_problem* P = nullptr;
+    struct NoRenumber {   // the local block keeps the user's row order (gofs mapping)
+        NoRenumber() { cpd::g_no_renumber = true; }
+        ~NoRenumber() { cpd::g_no_renumber = false; }
+    } nr_guard;
     if (partition == 1) {
         // columns [b0, b1): rows b0..b1 of CSR(A^T), global row indices of A
         std::vector<int32_t> p((size_t)(b1 - b0) + 1);

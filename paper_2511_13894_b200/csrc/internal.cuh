@@ -137,6 +137,11 @@ struct cpd_problem {
     int64_t L = 0;                   // slice length of the split side
     std::vector<int64_t> rank_gofs[2], rank_len[2];   // every rank's owned part (global)
     void* comm = nullptr;            // ncclComm_t (split >= 0)
+    // ---- hot-row renumbering: internal row k of A = user row rperm[k];
+    // the first `hot` internal rows are the longest (their y entries staged in smem)
+    cpd::DBuf<int32_t> rperm;
+    std::vector<int32_t> h_rperm;
+    int32_t hot = 0;
     // ---- short-row push: SELL(A^T) entries of short rows flagged
     bool push_on = false;
     int64_t push_nnz = 0;
@@ -239,6 +244,8 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
                  Gate g, double* red = nullptr);
 template <class Op>
 void launch_elem(Ctx& cx, int64_t N, const Op& op, Gate g, double* red = nullptr);
+
+extern thread_local bool g_no_renumber;   // set by cpd_problem_create_dist around the local create
 
 // diagonal preconditioning of a problem (problem.cu)
 void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc);

@@ -47,7 +47,8 @@ constexpr int HEAVY_MIN = 65536; // k_dense: rows with at least this many nonzer
 constexpr int HB = CPD_HB;       // k_dense: columns per dense block (64 KB of the vector in smem)
 constexpr int DCHUNK = 512;      // k_dense: entries per item (balances the Zipf head across warps)
 constexpr int TPB_D = 512;
-constexpr int FIN_SPLIT = 1024;  // k_finish: rows with more partials get a CTA, the rest a warp
+constexpr int FIN_SPLIT = 1024;
+constexpr int HOT_ROWS = 4096;   // y entries of the longest rows of A staged in k_sell's shared memory  // k_finish: rows with more partials get a CTA, the rest a warp
 
 enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2 };
 enum { ST_RUNNING = -1, ST_CONVERGED = 0, ST_ITER_LIMIT = 1, ST_TIME_LIMIT = 2, ST_FAIL = 3 };
@@ -871,6 +872,7 @@ struct DevSell {
     const double* __restrict__ val;
     int32_t rows, nslice;
     double* push = nullptr;   // acc (m) when this pass pushes its short-row products
+    int32_t hot = 0;          // gathered entries [0, hot) staged in shared memory (hot-row renumbering)
 };
 
 constexpr int TPB_SELL = 256;
@@ -912,6 +914,14 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
     const int lane = threadIdx.x & 31;
     const int nw = gridDim.x * (TPB_SELL / 32);
     __shared__ double vst[TPB_SELL / 32][(NVEC > 0 ? NVEC : 1) * 32];
+    // the gathered vector's hot prefix (the longest rows of A, most of the gathers)
+    extern __shared__ __align__(16) double yhot[];   // [NV][hot]
+    const int hot = M.hot;
+    for (int t = threadIdx.x; t < hot; t += TPB_SELL) {
+        yhot[t] = v0[t];
+        if (NV > 1) yhot[hot + t] = v1[t];
+    }
+    __syncthreads();
     // push only for an iteration the dual step will complete (k < k_stop)
     const bool push_on = M.push != nullptr && ctl->k < ctl->k_stop;
     for (int s = (blockIdx.x * TPB_SELL + threadIdx.x) >> 5; s < M.nslice; s += nw) {
@@ -951,8 +961,9 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
             double g[SELL_U], g2[SELL_U];
 #pragma unroll
             for (int u = 0; u < SELL_U; ++u) {
-                g[u] = c[u] >= 0 ? __ldg(&v0[c[u] & COL_MASK]) : 0.0;
-                if (NV > 1) g2[u] = c[u] >= 0 ? __ldg(&v1[c[u] & COL_MASK]) : 0.0;
+                const int cc = c[u] & COL_MASK;
+                g[u] = c[u] < 0 ? 0.0 : cc < hot ? yhot[cc] : __ldg(&v0[cc]);
+                if (NV > 1) g2[u] = c[u] < 0 ? 0.0 : cc < hot ? yhot[hot + cc] : __ldg(&v1[cc]);
             }
             int cn[SELL_U];
             double an[SELL_U];

@@ -388,6 +388,79 @@ void build_sell(Matrix& M, int64_t nnz, double max_ratio)
     S.on = true;
 }
 
+// ------------------------------------------------------------ hot-row renumbering
+// new row k of A = old row perm[k]: copy its entries (warp per row)
+__global__ void k_permute_rows(int32_t rows, const int32_t* perm, const int32_t* op, const int32_t* oj,
+                               const double* ox, const int32_t* np, int32_t* nj, double* nx)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < rows;
+         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t r = perm[k];
+        const int32_t a = op[r], len = op[r + 1] - a, d = np[k];
+        for (int32_t q = lane; q < len; q += 32) {
+            nj[d + q] = oj[a + q];
+            nx[d + q] = ox[a + q];
+        }
+    }
+}
+__global__ void k_remap(int64_t N, int32_t* j, const int32_t* pinv)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x)
+        j[q] = pinv[j[q]];
+}
+__global__ void k_gather_d(int64_t N, double* dst, const double* src, const int32_t* idx)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+thread_local bool g_no_renumber = false;
+
+// Rows of A ordered by decreasing length (stable) when the HOT_ROWS longest rows
+// hold >= 30% of the nonzeros (C5's Zipf rows): the most-gathered entries of y then
+// form a prefix that k_sell keeps in shared memory.  Every y-side
+// array is stored in this internal order; the ABI maps y / b / senses / r.
+static void renumber_rows(cpd_problem* P, std::vector<int32_t>& hp)
+{
+    const int32_t m = P->m;
+    const char* e = getenv("CPD_HOTROWS");
+    if ((e && e[0] == '0') || g_no_renumber || m <= HOT_ROWS || P->nnz == 0) return;
+    std::vector<int32_t> perm(m);
+    for (int32_t i = 0; i < m; ++i) perm[i] = i;
+    std::stable_sort(perm.begin(), perm.end(),
+                     [&](int32_t a, int32_t b) { return hp[a + 1] - hp[a] > hp[b + 1] - hp[b]; });
+    int64_t top = 0;
+    for (int32_t k = 0; k < HOT_ROWS; ++k) top += hp[perm[k] + 1] - hp[perm[k]];
+    if (10 * top < 3 * P->nnz) return;
+    const int sms = P->num_sms;
+    std::vector<int32_t> np((size_t)m + 1, 0), pinv(m);
+    for (int32_t k = 0; k < m; ++k) {
+        np[k + 1] = np[k] + (hp[perm[k] + 1] - hp[perm[k]]);
+        pinv[perm[k]] = k;
+    }
+    DBuf<int32_t> dperm(m), dpinv(m), dnp((size_t)m + 1), nj(std::max<int64_t>(P->nnz, 1));
+    DBuf<double> nx(std::max<int64_t>(P->nnz, 1)), nb(m);
+    CPD_CUDA(cudaMemcpy(dperm.p, perm.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice));
+    CPD_CUDA(cudaMemcpy(dpinv.p, pinv.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice));
+    CPD_CUDA(cudaMemcpy(dnp.p, np.data(), sizeof(int32_t) * ((size_t)m + 1), cudaMemcpyHostToDevice));
+    const int gw = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)m * 32 + 255) / 256, (int64_t)sms * 32));
+    k_permute_rows<<<gw, 256>>>(m, dperm.p, P->A.p.p, P->A.j.p, P->A.x.p, dnp.p, nj.p, nx.p);
+    auto grid = [&](int64_t N) { return (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, (int64_t)sms * 16)); };
+    k_remap<<<grid(P->nnz), 256>>>(P->nnz, P->AT.j.p, dpinv.p);
+    k_gather_d<<<grid(m), 256>>>(m, nb.p, P->b.p, dperm.p);
+    CPD_CUDA(cudaGetLastError());
+    CPD_CUDA(cudaDeviceSynchronize());
+    P->A.p = std::move(dnp);
+    P->A.j = std::move(nj);
+    P->A.x = std::move(nx);
+    CPD_CUDA(cudaMemcpy(P->b.p, nb.p, sizeof(double) * m, cudaMemcpyDeviceToDevice));
+    P->rperm = std::move(dperm);
+    P->h_rperm = perm;
+    P->hot = HOT_ROWS;
+    hp = np;
+}
+
 // ------------------------------------------------------------ validation
 // err[class] = smallest offending index (atomicMin), INT64_MAX if none.
 enum { ERR_ROWPTR = 0, ERR_COL = 1, ERR_ORDER = 2, ERR_VAL = 3, ERR_B = 4, ERR_C = 5, ERR_BND = 6,
@@ -784,6 +857,7 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         std::vector<int32_t> hp((size_t)m + 1), htp((size_t)n + 1);
         CPD_CUDA(cudaMemcpy(hp.data(), P->A.p.p, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
         CPD_CUDA(cudaMemcpy(htp.data(), P->AT.p.p, sizeof(int32_t) * htp.size(), cudaMemcpyDeviceToHost));
+        renumber_rows(P, hp);
         // A: warp-item plan for k_csrw unless CPD_WARP=0 (then the TMA plan of k_spmv)
         // default: warp plan when rows longer than WLONG carry >= 25% of the nonzeros
         // (C3, C5: measured faster); short-row matrices keep the TMA plan (C2, C4)

@@ -139,20 +139,28 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
                  Gate g, double* red)
 {
     if (M.sell.on) {
+        // A^T gathers y: its hot prefix (hot-row renumbering) is staged in shared memory
+        const int hot = (&M == &cx.P->AT) ? cx.P->hot : 0;
+        const size_t hsm = (size_t)NV * hot * sizeof(double);
         static int sgrid = 0, ssms = 0;
+        static size_t shsm = (size_t)-1;
         {
             std::lock_guard<std::mutex> lk(g_grid_mu);
-            if (!sgrid || ssms != cx.P->num_sms) {
+            if (!sgrid || ssms != cx.P->num_sms || shsm != hsm) {
+                CPD_CUDA(cudaFuncSetAttribute(k_sell<NV, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)hsm));
                 int nb = 0;
-                CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sell<NV, Epi>, TPB_SELL, 0));
+                CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sell<NV, Epi>, TPB_SELL, hsm));
                 ssms = cx.P->num_sms;
+                shsm = hsm;
                 sgrid = std::max(1, nb) * ssms;
             }
         }
         const int gr = std::max(1, std::min<int>(sgrid, (M.sell.nslice + 7) / 8));
         DevSell ds = M.dsell();
+        ds.hot = hot;
         if (PushRole<Epi>::v == 1) ds.push = cx.push_acc;
-        k_sell<NV, Epi><<<gr, TPB_SELL, 0, cx.st>>>(ds, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p, red);
+        k_sell<NV, Epi><<<gr, TPB_SELL, hsm, cx.st>>>(ds, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p, red);
         CPD_CUDA(cudaGetLastError());
         ++cx.launches;
         return;
@@ -525,6 +533,17 @@ __global__ void k_scale_vec(int64_t N, double* dst, const double* src, const dou
         dst[i] = op ? src[i] * d[i] : src[i] / d[i];
 }
 
+// internal row order <-> user order of y-side vectors (hot-row renumbering):
+// mode 0 gather dst[k] = src[perm[k]] (user -> internal); mode 1 scatter dst[perm[k]] = src[k]
+__global__ void k_perm_vec(int64_t N, double* dst, const double* src, const int32_t* perm, int mode)
+{
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (mode) dst[perm[k]] = src[k];
+        else dst[k] = src[perm[k]];
+    }
+}
+
 __global__ void k_zero(int64_t N, double* dst)
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
@@ -578,7 +597,7 @@ struct cpd_solver {
     Ctx cx;
     // state vectors: n-side (x-like) of length own_len[1], m-side (y-like) own_len[0]
     DBuf<double> X0, X1, Xa0, Xa1, Xr, Y, Ya, Yr, AX, AXa, Ystar, Z, lhat, uhat, chat, objd, SN, SM;
-    DBuf<double> LHo, UHo, TX, TY;   // scaled problems: original-space model bounds; unscale scratch
+    DBuf<double> LHo, UHo, TX, TY, TY2;   // scaled problems: original-space model bounds; unscale scratch
     DBuf<int8_t> shat;                // corner-model row senses
     DBuf<double> ACC;                 // short-row push sums (m), zero between iterations
     int64_t rows_eq = 0;
@@ -1048,8 +1067,15 @@ struct cpd_solver {
             else CPD_CUDA(cudaMemsetAsync(X0.p, 0, sizeof(double) * nO(), cx.st));
         }
         if (mO() > 0) {
-            if (y) CPD_CUDA(cudaMemcpyAsync(Y.p, y + P->gofs[0], sizeof(double) * mO(), kind, cx.st));
-            else CPD_CUDA(cudaMemsetAsync(Y.p, 0, sizeof(double) * mO(), cx.st));
+            if (y && P->hot) {   // user order -> internal row order
+                ensure_tmp();
+                CPD_CUDA(cudaMemcpyAsync(TY.p, y, sizeof(double) * mO(), kind, cx.st));
+                perm_vec(Y.p, TY.p, 0);
+            } else if (y) {
+                CPD_CUDA(cudaMemcpyAsync(Y.p, y + P->gofs[0], sizeof(double) * mO(), kind, cx.st));
+            } else {
+                CPD_CUDA(cudaMemsetAsync(Y.p, 0, sizeof(double) * mO(), cx.st));
+            }
         }
         if (P->scaled) {   // original-space input: x^ = x / s, y^ = y / r
             scale_vec(nO(), X0.p, X0.p, P->ss.p, 0);
@@ -1060,6 +1086,25 @@ struct cpd_solver {
         run_active = false;
         have_corner = false;
         eta_known = false;
+    }
+
+    void ensure_tmp()
+    {
+        if (!TX.p) {
+            TX.alloc(std::max(nO(), 1));
+            TY.alloc(std::max(mO(), 1));
+        }
+        if (P->hot && !TY2.p) TY2.alloc(std::max(mO(), 1));
+    }
+
+    void perm_vec(double* dst, const double* src, int mode)
+    {
+        const int64_t N = mO();
+        if (N <= 0) return;
+        const int g = (int)std::min<int64_t>(cx.grid_elem, (N + 255) / 256);
+        k_perm_vec<<<g, 256, 0, cx.st>>>(N, dst, src, P->rperm.p, mode);
+        CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
     }
 
     void scale_vec(int64_t N, double* dst, const double* src, const double* d, int op)
@@ -1110,14 +1155,22 @@ struct cpd_solver {
     {
         if (z) compute_z();
         const double *xs = Xp(cur_par), *ys = Y.p, *zs = Z.p;
-        if (P->scaled) {
-            if (!TX.p) {
-                TX.alloc(std::max(nO(), 1));
-                TY.alloc(std::max(mO(), 1));
+        if (P->scaled || P->hot) {
+            ensure_tmp();
+            if (x) {
+                if (P->scaled) scale_vec(nO(), TX.p, xs, P->ss.p, 1), xs = TX.p;
+                gather_full(1, xs, x, mem);
             }
-            if (x) scale_vec(nO(), TX.p, xs, P->ss.p, 1), xs = TX.p, gather_full(1, xs, x, mem);
-            if (y) scale_vec(mO(), TY.p, ys, P->sr.p, 1), ys = TY.p, gather_full(0, ys, y, mem);
-            if (z) scale_vec(nO(), TX.p, zs, P->is.p, 1), zs = TX.p, gather_full(1, zs, z, mem);
+            if (y) {
+                if (P->scaled) scale_vec(mO(), TY.p, ys, P->sr.p, 1), ys = TY.p;
+                if (P->hot) perm_vec(TY2.p, ys, 1), ys = TY2.p;   // internal -> user row order
+                gather_full(0, ys, y, mem);
+            }
+            if (z) {
+                cx.sync();   // TX reused
+                if (P->scaled) scale_vec(nO(), TX.p, zs, P->is.p, 1), zs = TX.p;
+                gather_full(1, zs, z, mem);
+            }
             cx.sync();
             return;
         }
@@ -1203,6 +1256,10 @@ int cpd_problem_set_senses(cpd_problem* p, const int8_t* sense, int32_t mem)
     else std::memcpy(h.data(), sense + off, (size_t)p->m);
     for (int64_t i = 0; i < p->m; ++i)
         if (h[i] < 0 || h[i] > 2) return fail(CPD_E_ARG, "row sense must be 0, 1 or 2 (row " + std::to_string(i + off) + ")");
+    if (p->hot) {   // user -> internal row order
+        std::vector<int8_t> t(h);
+        for (int64_t k = 0; k < p->m; ++k) h[k] = t[p->h_rperm[k]];
+    }
     CPD_CUDA(cudaSetDevice(p->device));
     p->sense.alloc(std::max<int32_t>(p->m, 1));
     CPD_CUDA(cudaMemcpy(p->sense.p, h.data(), (size_t)p->m, cudaMemcpyHostToDevice));
@@ -1227,7 +1284,13 @@ int cpd_problem_get_scaling(const cpd_problem* p, double* r, double* s)
     if (!p) return fail(CPD_E_ARG, "NULL problem");
     if (!p->scaled) return fail(CPD_E_STATE, "problem is not scaled");
     CPD_CUDA(cudaSetDevice(p->device));
-    if (r) CPD_CUDA(cudaMemcpy(r, p->sr.p, sizeof(double) * p->m, cudaMemcpyDeviceToHost));
+    if (r) {
+        CPD_CUDA(cudaMemcpy(r, p->sr.p, sizeof(double) * p->m, cudaMemcpyDeviceToHost));
+        if (p->hot) {   // internal -> user row order
+            std::vector<double> t(r, r + p->m);
+            for (int64_t k = 0; k < p->m; ++k) r[p->h_rperm[k]] = t[k];
+        }
+    }
     if (s) CPD_CUDA(cudaMemcpy(s, p->ss.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
     ABI_END
 }
@@ -1457,6 +1520,13 @@ int cpd_problem_score(const cpd_problem* p, const double* x, const double* y, in
     const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (nO) CPD_CUDA(cudaMemcpy(dx.p, x + p->gofs[1], sizeof(double) * nO, kind));
     if (mO) CPD_CUDA(cudaMemcpy(dy.p, y + p->gofs[0], sizeof(double) * mO, kind));
+    if (p->hot && mO) {   // user row order -> internal
+        DBuf<double> t(mO);
+        CPD_CUDA(cudaMemcpy(t.p, dy.p, sizeof(double) * mO, cudaMemcpyDeviceToDevice));
+        k_perm_vec<<<(int)std::min<int64_t>(4096, (mO + 255) / 256), 256, 0, cx.st>>>(mO, dy.p, t.p, p->rperm.p, 0);
+        CPD_CUDA(cudaGetLastError());
+        cx.sync();
+    }
     if (p->scaled) {   // original-space point -> scaled
         if (nO) k_scale_vec<<<(int)std::min<int64_t>(4096, (nO + 255) / 256), 256, 0, cx.st>>>(nO, dx.p, dx.p, p->ss.p, 0);
         if (mO) k_scale_vec<<<(int)std::min<int64_t>(4096, (mO + 255) / 256), 256, 0, cx.st>>>(mO, dy.p, dy.p, p->sr.p, 0);
