@@ -82,7 +82,9 @@ typedef struct cpd_solver cpd_solver;     /* owns iterate, workspace, stream, CU
  *  b[m], c[n] finite.  lb[n], ub[n]: NULL => lb = 0, ub = +inf; entries may be
  *  -inf / +inf respectively; lb_j <= ub_j.
  *  Validation runs on the device; on failure *out is untouched and the message
- *  names the first offending index. */
+ *  names the first offending index.  The library may store the rows of A in
+ *  another order internally (hot-row renumbering); every vector in or
+ *  out of the ABI is in the caller's order. */
 int cpd_problem_create(int32_t m, int32_t n, int64_t nnz,
                        const int32_t *A_rowptr, const int32_t *A_col, const double *A_val,
                        const int32_t *AT_rowptr, const int32_t *AT_col, const double *AT_val,
