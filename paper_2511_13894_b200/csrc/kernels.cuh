@@ -45,7 +45,10 @@ constexpr int HEAVY_MIN = 65536; // k_dense: rows with at least this many nonzer
 #define CPD_HB 8192
 #endif
 constexpr int HB = CPD_HB;       // k_dense: columns per dense block (64 KB of the vector in smem)
-constexpr int DCHUNK = 512;      // k_dense: entries per item (balances the Zipf head across warps)
+#ifndef CPD_DCHUNK
+#define CPD_DCHUNK 512
+#endif
+constexpr int DCHUNK = CPD_DCHUNK;   // k_dense: entries per item (balances the Zipf head across warps)
 constexpr int TPB_D = 512;
 constexpr int FIN_SPLIT = 1024;
 constexpr int HOT_ROWS = 4096;   // y entries of the longest rows of A staged in k_sell's shared memory  // k_finish: rows with more partials get a CTA, the rest a warp
