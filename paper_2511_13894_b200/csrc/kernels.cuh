@@ -34,8 +34,14 @@ constexpr int SINGLE_MIN = 256;  // a row with more nonzeros gets an entry of it
 constexpr int NSTAGE = 3;      // TMA pipeline depth (stages per CTA)
 constexpr int NVECMAX = 5;     // staged per-row vectors per entry
 constexpr int NSMAX = 12;      // max scalars an epilogue reduces
-constexpr int WCAP_ROWS = 1024;  // k_csrw: nonzeros per rows item (<= 32 rows)
-constexpr int WLONG = 512;       // k_csrw: a longer row is cut into pieces
+#ifndef CPD_WCAP_ROWS
+#define CPD_WCAP_ROWS 1024
+#endif
+#ifndef CPD_WLONG
+#define CPD_WLONG 512
+#endif
+constexpr int WCAP_ROWS = CPD_WCAP_ROWS;  // k_csrw: nonzeros per rows item (<= 32 rows)
+constexpr int WLONG = CPD_WLONG;          // k_csrw: a longer row is cut into pieces
 #ifndef CPD_WCAP_LONG
 #define CPD_WCAP_LONG 512
 #endif
