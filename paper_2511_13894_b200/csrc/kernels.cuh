@@ -38,7 +38,7 @@ constexpr int NSMAX = 12;      // max scalars an epilogue reduces
 #define CPD_WCAP_ROWS 1024
 #endif
 #ifndef CPD_WLONG
-#define CPD_WLONG 512
+#define CPD_WLONG 256
 #endif
 constexpr int WCAP_ROWS = CPD_WCAP_ROWS;  // k_csrw: nonzeros per rows item (<= 32 rows)
 constexpr int WLONG = CPD_WLONG;          // k_csrw: a longer row is cut into pieces

@@ -5,6 +5,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <functional>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -389,19 +390,20 @@ void build_sell(Matrix& M, int64_t nnz, double max_ratio)
 }
 
 // ------------------------------------------------------------ hot-row renumbering
-// new row k of A = old row perm[k]: copy its entries (warp per row)
-__global__ void k_permute_rows(int32_t rows, const int32_t* perm, const int32_t* op, const int32_t* oj,
-                               const double* ox, const int32_t* np, int32_t* nj, double* nx)
+// new row k of A = old row perm[k]: entry-parallel copy (a warp per row would leave
+// C5's 1.8e7-entry top row to one warp); the row of new position d by binary search
+__global__ void k_permute_rows(int32_t rows, int64_t nnz, const int32_t* perm, const int32_t* op,
+                               const int32_t* oj, const double* ox, const int32_t* np, int32_t* nj, double* nx)
 {
-    const int lane = threadIdx.x & 31;
-    for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < rows;
-         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int32_t r = perm[k];
-        const int32_t a = op[r], len = op[r + 1] - a, d = np[k];
-        for (int32_t q = lane; q < len; q += 32) {
-            nj[d + q] = oj[a + q];
-            nx[d + q] = ox[a + q];
+    for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < nnz; d += (int64_t)gridDim.x * blockDim.x) {
+        int32_t lo = 0, hi = rows;   // np[lo] <= d < np[hi]
+        while (hi - lo > 1) {
+            const int32_t mid = lo + (hi - lo) / 2;
+            if (np[mid] <= d) lo = mid; else hi = mid;
         }
+        const int64_t src = op[perm[lo]] + (d - np[lo]);
+        nj[d] = oj[src];
+        nx[d] = ox[src];
     }
 }
 __global__ void k_remap(int64_t N, int32_t* j, const int32_t* pinv)
@@ -421,44 +423,70 @@ thread_local bool g_no_renumber = false;
 // hold >= 30% of the nonzeros (C5's Zipf rows): the most-gathered entries of y then
 // form a prefix that k_sell keeps in shared memory.  Every y-side
 // array is stored in this internal order; the ABI maps y / b / senses / r.
+__global__ void k_len_keys(int32_t rows, const int32_t* p, int32_t maxlen, int32_t* key, int32_t* val)
+{
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        key[r] = maxlen - (p[r + 1] - p[r]);   // ascending key = descending length
+        val[r] = (int32_t)r;
+    }
+}
+__global__ void k_perm_lens(int32_t rows, const int32_t* perm, const int32_t* p, int32_t* len, int32_t* pinv)
+{
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < rows; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = perm[k];
+        len[k] = p[r + 1] - p[r];
+        pinv[r] = (int32_t)k;
+    }
+}
+
 static void renumber_rows(cpd_problem* P, std::vector<int32_t>& hp)
 {
     const int32_t m = P->m;
     const char* e = getenv("CPD_HOTROWS");
     if ((e && e[0] == '0') || g_no_renumber || m <= HOT_ROWS || P->nnz == 0) return;
-    std::vector<int32_t> perm(m);
-    for (int32_t i = 0; i < m; ++i) perm[i] = i;
-    std::stable_sort(perm.begin(), perm.end(),
-                     [&](int32_t a, int32_t b) { return hp[a + 1] - hp[a] > hp[b + 1] - hp[b]; });
+    // cheap host test first: do the HOT_ROWS longest rows hold >= 30% of the nonzeros?
+    int32_t maxlen = 0;
+    std::vector<int32_t> lens(m);
+    for (int32_t i = 0; i < m; ++i) {
+        lens[i] = hp[i + 1] - hp[i];
+        maxlen = std::max(maxlen, lens[i]);
+    }
+    std::nth_element(lens.begin(), lens.begin() + HOT_ROWS, lens.end(), std::greater<int32_t>());
     int64_t top = 0;
-    for (int32_t k = 0; k < HOT_ROWS; ++k) top += hp[perm[k] + 1] - hp[perm[k]];
+    for (int32_t k = 0; k < HOT_ROWS; ++k) top += lens[k];
     if (10 * top < 3 * P->nnz) return;
     const int sms = P->num_sms;
-    std::vector<int32_t> np((size_t)m + 1, 0), pinv(m);
-    for (int32_t k = 0; k < m; ++k) {
-        np[k + 1] = np[k] + (hp[perm[k] + 1] - hp[perm[k]]);
-        pinv[perm[k]] = k;
-    }
-    DBuf<int32_t> dperm(m), dpinv(m), dnp((size_t)m + 1), nj(std::max<int64_t>(P->nnz, 1));
-    DBuf<double> nx(std::max<int64_t>(P->nnz, 1)), nb(m);
-    CPD_CUDA(cudaMemcpy(dperm.p, perm.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice));
-    CPD_CUDA(cudaMemcpy(dpinv.p, pinv.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice));
-    CPD_CUDA(cudaMemcpy(dnp.p, np.data(), sizeof(int32_t) * ((size_t)m + 1), cudaMemcpyHostToDevice));
-    const int gw = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)m * 32 + 255) / 256, (int64_t)sms * 32));
-    k_permute_rows<<<gw, 256>>>(m, dperm.p, P->A.p.p, P->A.j.p, P->A.x.p, dnp.p, nj.p, nx.p);
     auto grid = [&](int64_t N) { return (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, (int64_t)sms * 16)); };
+    // stable device sort by decreasing length (radix sort is stable)
+    DBuf<int32_t> key(m), key2(m), val(m), dperm(m), dpinv(m), nlen((size_t)m + 1), dnp((size_t)m + 1);
+    k_len_keys<<<grid(m), 256>>>(m, P->A.p.p, maxlen, key.p, val.p);
+    int end_bit = 1;
+    while ((1LL << end_bit) <= (long long)maxlen) ++end_bit;
+    size_t tb = 0;
+    CPD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, val.p, dperm.p, m, 0, end_bit));
+    DBuf<unsigned char> tmp(tb);
+    CPD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key2.p, val.p, dperm.p, m, 0, end_bit));
+    k_perm_lens<<<grid(m), 256>>>(m, dperm.p, P->A.p.p, nlen.p, dpinv.p);
+    CPD_CUDA(cudaMemset(nlen.p + m, 0, sizeof(int32_t)));
+    size_t sb = 0;
+    CPD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, nlen.p, dnp.p, m + 1));
+    DBuf<unsigned char> stmp(sb);
+    CPD_CUDA(cub::DeviceScan::ExclusiveSum(stmp.p, sb, nlen.p, dnp.p, m + 1));
+    DBuf<int32_t> nj(std::max<int64_t>(P->nnz, 1));
+    DBuf<double> nx(std::max<int64_t>(P->nnz, 1)), nb(m);
+    k_permute_rows<<<grid(P->nnz), 256>>>(m, P->nnz, dperm.p, P->A.p.p, P->A.j.p, P->A.x.p, dnp.p, nj.p, nx.p);
     k_remap<<<grid(P->nnz), 256>>>(P->nnz, P->AT.j.p, dpinv.p);
     k_gather_d<<<grid(m), 256>>>(m, nb.p, P->b.p, dperm.p);
     CPD_CUDA(cudaGetLastError());
-    CPD_CUDA(cudaDeviceSynchronize());
+    P->h_rperm.resize(m);
+    CPD_CUDA(cudaMemcpy(P->h_rperm.data(), dperm.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+    CPD_CUDA(cudaMemcpy(hp.data(), dnp.p, sizeof(int32_t) * ((size_t)m + 1), cudaMemcpyDeviceToHost));
+    CPD_CUDA(cudaMemcpy(P->b.p, nb.p, sizeof(double) * m, cudaMemcpyDeviceToDevice));
     P->A.p = std::move(dnp);
     P->A.j = std::move(nj);
     P->A.x = std::move(nx);
-    CPD_CUDA(cudaMemcpy(P->b.p, nb.p, sizeof(double) * m, cudaMemcpyDeviceToDevice));
     P->rperm = std::move(dperm);
-    P->h_rperm = perm;
     P->hot = HOT_ROWS;
-    hp = np;
 }
 
 // ------------------------------------------------------------ validation
@@ -653,14 +681,15 @@ static void validate_csr(int32_t rows, int32_t cols, int64_t nnz, const Matrix& 
 
 namespace cpd {
 // ------------------------------------------------------------ diagonal preconditioning
-// per row of a CSR layout: max |a| (mode 0) or sum |a| (mode 1); warp per row
+// per row of a CSR layout: max |a| (mode 0) or sum |a| (mode 1), then sqrt (1 if 0);
+// a CTA per row (strided per thread, block tree: fixed order), so long rows do not
+// serialise on one warp
 __global__ void k_row_absred(int32_t rows, const int32_t* p, const double* x, int mode, double* out)
 {
-    const int lane = threadIdx.x & 31;
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
-         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    __shared__ double sw[8];
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         double v = 0.0;
-        for (int64_t q = p[r] + lane; q < p[r + 1]; q += 32) {
+        for (int64_t q = p[r] + threadIdx.x; q < p[r + 1]; q += blockDim.x) {
             const double a = fabs(x[q]);
             v = mode ? v + a : (a > v ? a : v);
         }
@@ -668,22 +697,32 @@ __global__ void k_row_absred(int32_t rows, const int32_t* p, const double* x, in
             const double t = __shfl_xor_sync(0xffffffffu, v, o);
             v = mode ? v + t : (t > v ? t : v);
         }
-        if (lane == 0) out[r] = v > 0.0 ? sqrt(v) : 1.0;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = mode ? t + sw[w] : (sw[w] > t ? sw[w] : t);
+            out[r] = t > 0.0 ? sqrt(t) : 1.0;
+        }
     }
 }
 
 // x_q <- x_q / (rho_i kappa_j) for entry q of row `r`, column `c` of a layout:
 // A (swap 0): rho = rs[r], kappa = cs[c];  A^T (swap 1): rho = cs[c], kappa = rs[r]
-__global__ void k_apply_scale(int32_t rows, const int32_t* p, const int32_t* j, double* x, const double* rs,
-                              const double* cs, int swap)
+// (entry-parallel; the row of entry q by binary search)
+__global__ void k_apply_scale(int32_t rows, int64_t nnz, const int32_t* p, const int32_t* j, double* x,
+                              const double* rs, const double* cs, int swap)
 {
-    const int lane = threadIdx.x & 31;
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
-         r += ((int64_t)gridDim.x * blockDim.x) >> 5)
-        for (int64_t q = p[r] + lane; q < p[r + 1]; q += 32) {
-            const double den = swap ? cs[j[q]] * rs[r] : rs[r] * cs[j[q]];
-            x[q] = x[q] / den;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x) {
+        int32_t lo = 0, hi = rows;
+        while (hi - lo > 1) {
+            const int32_t mid = lo + (hi - lo) / 2;
+            if (p[mid] <= q) lo = mid; else hi = mid;
         }
+        const double den = swap ? cs[j[q]] * rs[lo] : rs[lo] * cs[j[q]];
+        x[q] = x[q] / den;
+    }
 }
 
 // op 0: v /= d; op 1: v *= d; op 2: out = 1 / v
@@ -702,7 +741,7 @@ void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc)
 {
     const int32_t m = P->m, n = P->n;
     const int sms = P->num_sms;
-    auto gw = [&](int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>((rows * 32 + 255) / 256, (int64_t)sms * 32)); };
+    auto gr = [&](int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)sms * 64)); };
     P->sr.alloc(m);
     P->ss.alloc(n);
     P->ir.alloc(m);
@@ -712,10 +751,10 @@ void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc)
     k_fill<<<grid_of(n, sms), 256>>>(n, P->ss.p, 1.0);
     for (int pass = 0; pass < ruiz_iters + (pc ? 1 : 0); ++pass) {
         const int mode = pass >= ruiz_iters ? 1 : 0;
-        k_row_absred<<<gw(m), 256>>>(m, P->A.p.p, P->A.x.p, mode, rho.p);
-        k_row_absred<<<gw(n), 256>>>(n, P->AT.p.p, P->AT.x.p, mode, kap.p);
-        k_apply_scale<<<gw(m), 256>>>(m, P->A.p.p, P->A.j.p, P->A.x.p, rho.p, kap.p, 0);
-        k_apply_scale<<<gw(n), 256>>>(n, P->AT.p.p, P->AT.j.p, P->AT.x.p, kap.p, rho.p, 1);
+        k_row_absred<<<gr(m), 256>>>(m, P->A.p.p, P->A.x.p, mode, rho.p);
+        k_row_absred<<<gr(n), 256>>>(n, P->AT.p.p, P->AT.x.p, mode, kap.p);
+        k_apply_scale<<<grid_of(P->nnz, sms), 256>>>(m, P->nnz, P->A.p.p, P->A.j.p, P->A.x.p, rho.p, kap.p, 0);
+        k_apply_scale<<<grid_of(P->nnz, sms), 256>>>(n, P->nnz, P->AT.p.p, P->AT.j.p, P->AT.x.p, kap.p, rho.p, 1);
         k_vec_op<<<grid_of(m, sms), 256>>>(m, P->sr.p, rho.p, 0, nullptr);
         k_vec_op<<<grid_of(n, sms), 256>>>(n, P->ss.p, kap.p, 0, nullptr);
         CPD_CUDA(cudaGetLastError());
