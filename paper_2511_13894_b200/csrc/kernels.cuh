@@ -38,7 +38,7 @@ constexpr int NSMAX = 12;      // max scalars an epilogue reduces
 #define CPD_WCAP_ROWS 1024
 #endif
 #ifndef CPD_WLONG
-#define CPD_WLONG 256
+#define CPD_WLONG 128
 #endif
 constexpr int WCAP_ROWS = CPD_WCAP_ROWS;  // k_csrw: nonzeros per rows item (<= 32 rows)
 constexpr int WLONG = CPD_WLONG;          // k_csrw: a longer row is cut into pieces
@@ -889,7 +889,7 @@ constexpr int TPB_SELL = 256;
 #define CPD_PRE 0   // 1: epilogue inputs held in registers across the sum (more registers)
 #endif
 #ifndef CPD_SELL_U
-#define CPD_SELL_U 8
+#define CPD_SELL_U 6
 #endif
 constexpr int SELL_U = CPD_SELL_U;   // entries per lane in flight
 
