@@ -1225,9 +1225,23 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
 #define CPD_DU 8
 #endif
     constexpr int DU = CPD_DU;
-    for (int blk = blockIdx.x; blk < P.nhb; blk += gridDim.x) {
+    // balanced at item granularity: CTA c takes items [c I / G, (c + 1) I / G) (sorted by
+    // column block) and loads each block of the vector its range touches
+    const int64_t I = P.dense_ptr[P.nhb];
+    const int ia = (int)(I * blockIdx.x / gridDim.x), ib = (int)(I * (blockIdx.x + 1) / gridDim.x);
+    int blk = 0;
+    {
+        int lo = 0, hi = P.nhb;   // last block with dense_ptr[blk] <= ia
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (P.dense_ptr[mid] <= ia) lo = mid; else hi = mid;
+        }
+        blk = lo;
+    }
+    for (; blk < P.nhb && P.dense_ptr[blk] < ib; ++blk) {
         const int j0 = blk * HB, nj = min(HB, cols - j0);
-        const int i0 = P.dense_ptr[blk], i1 = P.dense_ptr[blk + 1];
+        const int i0 = max(P.dense_ptr[blk], ia), i1 = min(P.dense_ptr[blk + 1], ib);
+        if (i1 <= i0) continue;
         __syncthreads();
         for (int t = threadIdx.x; t < nj; t += TPB_D) {
             xs[t] = v0[j0 + t];

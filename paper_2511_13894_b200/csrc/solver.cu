@@ -201,7 +201,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
                         dgrid = std::max(1, nb) * dsms;
                     }
                 }
-                const int grd = std::max(1, std::min(dgrid, dp.nhb));
+                const int grd = std::max(1, dgrid);   // item-balanced: every CTA busy
                 k_dense<NV><<<grd, TPB_D, DSM, cx.st>>>(M.dev(), dp, M.cols, v0, v1, g0, cx.ctl);
                 CPD_CUDA(cudaGetLastError());
                 ++cx.launches;
