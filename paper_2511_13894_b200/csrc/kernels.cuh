@@ -57,6 +57,7 @@ constexpr int HB = CPD_HB;       // k_dense: columns per dense block (64 KB of t
 constexpr int DCHUNK = CPD_DCHUNK;   // k_dense: entries per item (balances the Zipf head across warps)
 constexpr int TPB_D = 512;
 constexpr int FIN_SPLIT = 1024;
+constexpr int TPB_F = 1024;      // k_finish threads per CTA (a CTA per heavy row)
 constexpr int HOT_ROWS = 4096;   // y entries of the longest rows of A staged in k_sell's shared memory  // k_finish: rows with more partials get a CTA, the rest a warp
 
 enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2 };
@@ -780,13 +781,13 @@ k_spmv(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
 // row sum, then combines this kernel's block partials with those k_spmv left
 // (first `prev` slots) and finalizes.
 template <int NV, class Epi>
-__global__ void __launch_bounds__(TPB)
+__global__ void __launch_bounds__(TPB_F)
 k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, int prev, double* red)
 {
     constexpr int NS = Epi::NS;
     constexpr int NVEC = Epi::NVEC;
     __shared__ int s_go;
-    __shared__ double s_w[TPB / 32][NV];
+    __shared__ double s_w[TPB_F / 32][NV];
     if (threadIdx.x == 0) s_go = gate_open(gate, ctl);
     __syncthreads();
     if (!s_go) return;
@@ -814,19 +815,19 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
 #pragma unroll
             for (int v = 0; v < NV; ++v) a8[u][v] = 0.0;
         int64_t t = t0 + threadIdx.x;
-        for (; t + 7 * TPB < t1; t += 8 * TPB)
+        for (; t + 7 * TPB_F < t1; t += 8 * TPB_F)
 #pragma unroll
             for (int u = 0; u < 8; ++u)
 #pragma unroll
-                for (int v = 0; v < NV; ++v) a8[u][v] += __ldcg(&P.lpart[(t + u * TPB) * 2 + v]);
-        for (int u = 0; t < t1; t += TPB, ++u)
+                for (int v = 0; v < NV; ++v) a8[u][v] += __ldcg(&P.lpart[(t + u * TPB_F) * 2 + v]);
+        for (int u = 0; t < t1; t += TPB_F, ++u)
 #pragma unroll
             for (int v = 0; v < NV; ++v) a8[u & 7][v] += __ldcg(&P.lpart[t * 2 + v]);
 #pragma unroll
         for (int u = 0; u < 8; ++u)
 #pragma unroll
             for (int v = 0; v < NV; ++v) sm[v] += a8[u][v];
-        block_sum<NV>(sm, s_w);
+        block_sum<NV, TPB_F>(sm, s_w);
         if (threadIdx.x == 0) {
             const int r = P.long_row[l];
             e.row(r, sm, vin, r, acc);
@@ -834,8 +835,8 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
     }
     {
         const int lane = threadIdx.x & 31;
-        const int nw = gridDim.x * (TPB / 32);
-        for (int h = P.nfin_heavy + ((blockIdx.x * TPB + threadIdx.x) >> 5); h < P.nlong; h += nw) {
+        const int nw = gridDim.x * (TPB_F / 32);
+        for (int h = P.nfin_heavy + ((blockIdx.x * TPB_F + threadIdx.x) >> 5); h < P.nlong; h += nw) {
             const int l = P.long_ents[h];
             double sm[NV];
 #pragma unroll
@@ -854,7 +855,7 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
             }
         }
     }
-    grid_finalize<NS>(acc, bpart, ctr, prev, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+    grid_finalize<NS, TPB_F>(acc, bpart, ctr, prev, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
 }
 
 // ------------------------------------------------------------ SELL-32 SpMV + epilogue
