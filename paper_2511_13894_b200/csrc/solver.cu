@@ -253,7 +253,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
             if (seg.size() < 3) launch_dense();
         }
         if (dp.nlong > 0) {
-            const int gf = std::max(1, std::min(cx.P->num_sms * 2, std::max(dp.nfin_heavy, (dp.nlong + TPB_F / 32 - 1) / (TPB_F / 32))));
+            const int gf = std::max(1, std::min(cx.P->num_sms * 8, std::max(dp.nfin_heavy, (dp.nlong + TPB_F / 32 - 1) / (TPB_F / 32))));
             Gate g2 = g;
             g2.active = nullptr;
             k_finish<NV, Epi><<<gf, TPB_F, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, prev, red);
@@ -282,7 +282,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
     CPD_CUDA(cudaGetLastError());
     ++cx.launches;
     if (dp.nlong > 0) {
-        const int gf = std::max(1, std::min(cx.P->num_sms * 2, std::max(dp.nfin_heavy, (dp.nlong + TPB_F / 32 - 1) / (TPB_F / 32))));
+        const int gf = std::max(1, std::min(cx.P->num_sms * 8, std::max(dp.nfin_heavy, (dp.nlong + TPB_F / 32 - 1) / (TPB_F / 32))));
         Gate g2 = g;
         g2.active = nullptr;
         k_finish<NV, Epi><<<gf, TPB_F, 0, cx.st>>>(dp, epi, g2, cx.ctl, cx.bpart.p, cx.ctr.p, gr, red);
