@@ -216,14 +216,14 @@ def reference_arm(args, lp, rank, world):
     }
 
 
-def workload_config(args, lp, world):
+def workload_config(args, lp, world, part=None):
     return {"workload": f"{lp.name}: BASELINE.json config 5 (m={lp.m}, n={lp.n}, nnz={lp.nnz}, Zipf(1.2) rows)"
             if lp.name == "c5" else f"{lp.name} (m={lp.m}, n={lp.n}, nnz={lp.nnz})",
             "m": lp.m, "n": lp.n, "nnz": lp.nnz, "seed": lp.meta.get("seed"),
             "step": f"set_iterate(0) + cpd_solve(max_iters={args.iters1}, eps_rel=1e-4) + "
                     f"cpd_corner_push(max_iters={args.iters2})",
             "l2": "inputs larger than L2 (matrix 5.9 GB vs 126 MB L2)" if lp.nnz > 1e7 else "no flush",
-            "parallelism": f"row-block x{world}" if world > 1 else "1 GPU"}
+            "parallelism": (f"{part} x{world}" if part else "1 GPU")}
 
 
 def cpu_baseline(lp):
@@ -336,7 +336,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded lpgen, BASELINE.json config recipe)",
-        "config": workload_config(args, lp, world),
+        "config": workload_config(args, lp, world,
+                                  {0: "row-block", 1: "col-block"}.get(P_info["partition"]) if dist_path else None),
         "hbm_gbs_model": hbm_gbs,
         "iterations_per_step": {"phase1": it1, "corner": it2},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
