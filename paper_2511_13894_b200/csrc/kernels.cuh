@@ -55,7 +55,10 @@ constexpr int HB = CPD_HB;       // k_dense: columns per dense block (64 KB of t
 #define CPD_DCHUNK 512
 #endif
 constexpr int DCHUNK = CPD_DCHUNK;   // k_dense: entries per item (balances the Zipf head across warps)
-constexpr int TPB_D = 512;
+#ifndef CPD_TPB_D
+#define CPD_TPB_D 512
+#endif
+constexpr int TPB_D = CPD_TPB_D;
 constexpr int FIN_SPLIT = 1024;
 constexpr int TPB_F = 256;       // k_finish threads per CTA (1024 measured slower: 52 vs 45 us)
 constexpr int HOT_ROWS = 4096;   // y entries of the longest rows of A staged in k_sell's shared memory  // k_finish: rows with more partials get a CTA, the rest a warp
