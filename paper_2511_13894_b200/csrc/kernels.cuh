@@ -1,14 +1,20 @@
 // kernels.cuh — sm_100a device code for the R-PDHG + corner-push hot path.
 //
-// One kernel template does all sparse work: k_spmv<NV, Epi> walks a precomputed
-// nnz-balanced PLAN of a CSR matrix (A or A^T), forms NV row sums of gathered
-// vectors, and hands every finished row to a fused epilogue (the PDHG primal or
-// dual step, the restart-check evaluations, the power iteration, the corner-model
-// setup).  Epilogues accumulate the scalars the method needs (norms, dots,
-// counts) in registers; a deterministic block reduction and a last-block-done
-// grid combine turn them into totals, and the last block runs the epilogue's
-// `finalize` (termination / restart / step-size decisions) ON THE DEVICE, so the
-// host never synchronises inside a batch of iterations.
+// Every sparse pass forms NV row sums of gathered vectors and hands each finished
+// row to a fused epilogue (the PDHG primal or dual step, the restart-check
+// evaluations, the power iteration, the corner-model setup, the split-product
+// store).  Three engines stream the matrix:
+//   k_sell   SELL-32 copy of a short-row layout (A^T): warp = 32 rows, lane = row,
+//            coalesced streaming, L1 / shared-memory gathers;
+//   k_csrw   warp items of a CSR plan (A with long rows): rows items via a segmented
+//            warp scan, long-row pieces per column slab, k_dense for the heavy rows
+//            by dense column blocks in shared memory, k_finish per long row;
+//   k_spmv   the persistent TMA (cp.async.bulk + mbarrier) ring for other CSR plans.
+// Epilogues accumulate the scalars the method needs (norms, dots, counts) in
+// registers; a deterministic block reduction and a last-block-done grid combine
+// turn them into totals, and the last block runs the epilogue's `finalize`
+// (termination / restart / step-size decisions) ON THE DEVICE, so the host never
+// synchronises inside a batch of iterations.
 //
 // Paper mapping (PAPER.md lines):
 //   EpiPrimal  a2 + a5 + a6(n-side): x+ = proj(x - tau (c - A^T y)), x_avg, c^T x,
@@ -17,8 +23,9 @@
 //              ||b - A x+||^2, b^T y+                           (BJ north_star)
 //   EpiCheckN/M  a7: KKT of current and average, restart decision, omega update
 //   EpiCorner  a8: z = c - A^T y, Algorithm 1 bound map, Uniform objective
-//   k_stats    a10: off-bound / zero-reduced-cost / candidate counts
-// Deterministic: every sum is taken in a fixed order for a fixed grid.
+//   OpStats    a10: off-bound / zero-reduced-cost / candidate counts
+// Deterministic: every sum is taken in a fixed order for a fixed grid (the opt-in
+// short-row push, CPD_PUSH=1, is the one exception: fp64 atomics).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
