@@ -20,6 +20,9 @@ namespace cpd {
 // Column slab width for long-row pieces: 4M columns = 32 MB of the gathered fp64
 // vector, so the slab being swept stays resident in the 126 MB L2.
 constexpr int64_t SLAB_COLS = 4 << 20;
+#ifndef CPD_SLAB_MIN
+#define CPD_SLAB_MIN 0   // long rows shorter than this are not cut at column-slab boundaries
+#endif
 #ifndef CPD_SHORT_SLABS
 #define CPD_SHORT_SLABS 2   // short rows (CPD_SHORT=1): column slabs of n / 2 (80 MB of C5's x each)
 #endif
@@ -147,6 +150,16 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
         if (is_heavy[l]) continue;
         const int32_t r = lrows[l];
         int32_t a = rp[r];
+        if ((int64_t)rp[r + 1] - rp[r] < CPD_SLAB_MIN) {
+            // too short to profit from slab cuts (they would leave tiny pieces): plain
+            // pieces, listed with the slab of the row's middle entry
+            const int32_t mid = std::min<int32_t>(nslab - 1, nb > 0 ? (int32_t)(std::lower_bound(
+                pos.begin() + (size_t)l * nb, pos.begin() + (size_t)(l + 1) * nb, (a + rp[r + 1]) / 2 + 1) -
+                (pos.begin() + (size_t)l * nb)) : 0);
+            for (int32_t q = a; q < rp[r + 1]; q += (int32_t)piece)
+                by_slab[mid].push_back(PlanEntry{r, -1 - l, q, (int32_t)std::min<int64_t>((int64_t)q + piece, rp[r + 1])});
+            continue;
+        }
         for (int32_t s = 0; s < nslab; ++s) {
             const int32_t b = (s + 1 < nslab) ? pos[(size_t)l * nb + s] : rp[r + 1];
             for (int32_t q = a; q < b; q += (int32_t)piece)
