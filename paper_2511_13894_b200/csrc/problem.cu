@@ -19,7 +19,10 @@ namespace cpd {
 // ------------------------------------------------------------------ plans
 // Column slab width for long-row pieces: 4M columns = 32 MB of the gathered fp64
 // vector, so the slab being swept stays resident in the 126 MB L2.
-constexpr int64_t SLAB_COLS = 4 << 20;
+#ifndef CPD_SLAB_COLS
+#define CPD_SLAB_COLS (4 << 20)
+#endif
+constexpr int64_t SLAB_COLS = CPD_SLAB_COLS;
 #ifndef CPD_SLAB_MIN
 #define CPD_SLAB_MIN 0   // long rows shorter than this are not cut at column-slab boundaries
 #endif
