@@ -5,6 +5,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <functional>
 #include <cstdlib>
 #include <cmath>
@@ -811,12 +813,28 @@ void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc)
 using namespace cpd;
 
 // Implementation of cpd_problem_create (called from the ABI layer).
+// CPD_TIMING=1: per-phase wall time of problem creation on stderr (device synchronised)
+struct PhaseTimer {
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    PhaseTimer() : on(getenv("CPD_TIMING") && getenv("CPD_TIMING")[0] == '1'), t(std::chrono::steady_clock::now()) {}
+    void mark(const char* what)
+    {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[cpd create] %-22s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const int32_t* Ap,
                                      const int32_t* Aj, const double* Ax, const int32_t* ATp,
                                      const int32_t* ATj, const double* ATx, const double* b,
                                      const double* c, const double* lb, const double* ub,
                                      int32_t mem, int32_t device)
 {
+    PhaseTimer tm;
     if (m < 1 || n < 1 || nnz < 0 || nnz >= (1LL << 31))
         throw Error(CPD_E_DIM, "need m >= 1, n >= 1, 0 <= nnz < 2^31");
     if (mem != CPD_HOST && mem != CPD_DEVICE) throw Error(CPD_E_ARG, "mem must be CPD_HOST or CPD_DEVICE");
@@ -864,12 +882,14 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
             upload(P->AT.x, ATx, (size_t)nnz, mem);
             validate_csr(n, m, nnz, P->AT, err, sms);
         }
+        tm.mark("upload+validate");
         Matrix* other = haveA ? &P->AT : &P->A;
         other->p.alloc((size_t)other->rows + 1);
         other->j.alloc(std::max<int64_t>(nnz, 1));
         other->x.alloc(std::max<int64_t>(nnz, 1));
         transpose(given->rows, given->cols, nnz, given->p.p, given->j.p, given->x.p, other->p.p,
                   other->j.p, other->x.p, sms);
+        tm.mark("transpose");
         if (haveA && haveAT) {
             // compare the caller's CSR(A^T) with the device transpose of CSR(A), bit for bit
             Matrix T;
@@ -908,11 +928,14 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
             CPD_CUDA(cudaMemcpy(&P->l0, P->lb.p, sizeof(double), cudaMemcpyDeviceToHost));
             CPD_CUDA(cudaMemcpy(&P->u0, P->ub.p, sizeof(double), cudaMemcpyDeviceToHost));
         }
+        tm.mark("vectors+bounds");
         // SpMV plans (host pass over the row pointers)
         std::vector<int32_t> hp((size_t)m + 1), htp((size_t)n + 1);
         CPD_CUDA(cudaMemcpy(hp.data(), P->A.p.p, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
         CPD_CUDA(cudaMemcpy(htp.data(), P->AT.p.p, sizeof(int32_t) * htp.size(), cudaMemcpyDeviceToHost));
+        tm.mark("rowptr D2H");
         renumber_rows(P, hp);
+        tm.mark("renumber");
         // A: warp-item plan for k_csrw unless CPD_WARP=0 (then the TMA plan of k_spmv)
         // default: warp plan when rows longer than WLONG carry >= 25% of the nonzeros
         // (C3, C5: measured faster); short-row matrices keep the TMA plan (C2, C4)
@@ -925,13 +948,16 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         bool warpA = 4 * long_nnz >= nnz && nnz > 0;
         if (we) warpA = we[0] != '0';
         build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.x.p, P->A.plan, warpA);
+        tm.mark("plan A");
         build_plan(n, m, htp, P->AT.p.p, P->AT.j.p, P->AT.x.p, P->AT.plan);
+        tm.mark("plan AT");
         // SELL-32 where the rows are short and even (padding <= 25%); CPD_SELL=0 disables
         const char* se = getenv("CPD_SELL");
         const bool sell_ok = !(se && se[0] == '0');
         // (A^T only: for A the dual epilogue's four staged vectors favour the TMA plan
         // kernel, measured on C4 — profiles/r01_kernel_iterations.md)
         if (sell_ok && nnz <= (int64_t)n * 64) build_sell(P->AT, nnz, 1.25);
+        tm.mark("sell");
         mark_push(P);
         CPD_CUDA(cudaDeviceSynchronize());
     } catch (...) {
