@@ -932,7 +932,6 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         // SpMV plans (host pass over the row pointers)
         std::vector<int32_t> hp((size_t)m + 1), htp((size_t)n + 1);
         CPD_CUDA(cudaMemcpy(hp.data(), P->A.p.p, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
-        CPD_CUDA(cudaMemcpy(htp.data(), P->AT.p.p, sizeof(int32_t) * htp.size(), cudaMemcpyDeviceToHost));
         tm.mark("rowptr D2H");
         renumber_rows(P, hp);
         tm.mark("renumber");
@@ -949,8 +948,6 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         if (we) warpA = we[0] != '0';
         build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.x.p, P->A.plan, warpA);
         tm.mark("plan A");
-        build_plan(n, m, htp, P->AT.p.p, P->AT.j.p, P->AT.x.p, P->AT.plan);
-        tm.mark("plan AT");
         // SELL-32 where the rows are short and even (padding <= 25%); CPD_SELL=0 disables
         const char* se = getenv("CPD_SELL");
         const bool sell_ok = !(se && se[0] == '0');
@@ -958,6 +955,14 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         // kernel, measured on C4 — profiles/r01_kernel_iterations.md)
         if (sell_ok && nnz <= (int64_t)n * 64) build_sell(P->AT, nnz, 1.25);
         tm.mark("sell");
+        // every A^T pass runs on SELL when it is on: its TMA plan is only needed otherwise
+        if (!P->AT.sell.on) {
+            CPD_CUDA(cudaMemcpy(htp.data(), P->AT.p.p, sizeof(int32_t) * htp.size(), cudaMemcpyDeviceToHost));
+            build_plan(n, m, htp, P->AT.p.p, P->AT.j.p, P->AT.x.p, P->AT.plan);
+        } else {
+            P->AT.plan.seg.assign(2, 0);
+        }
+        tm.mark("plan AT");
         mark_push(P);
         CPD_CUDA(cudaDeviceSynchronize());
     } catch (...) {
