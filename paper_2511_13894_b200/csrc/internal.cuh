@@ -72,9 +72,10 @@ struct Plan {
     DBuf<PlanEntry> dense_ent;            // {slot, block, q0, q1} grouped by block
     DBuf<int32_t> dense_ptr;              // [nhb + 1] item range of each block
     int32_t dense_maxitems = 0;           // most items in one block (k_dense smem)
-    // short rows by column slab (k_short): [nslab][rows + 1] pointers, entries slab-major
+    // short rows by column slab (k_csrw slab mode): [nslab][rows + 1] pointers, entries slab-major
     int32_t short_on = 0;
     int32_t short_nslab = 1;
+    int32_t short_ilv = 0;      // short slabs == piece slabs: interleave the passes
     int64_t short_width = 0;
     int64_t short_nnz = 0;
     DBuf<int32_t> short_ptr, short_col;

@@ -53,7 +53,10 @@ constexpr int WLONG = CPD_WLONG;          // k_csrw: a longer row is cut into pi
 #define CPD_WCAP_LONG 512
 #endif
 constexpr int WCAP_LONG = CPD_WCAP_LONG;  // k_csrw: nonzeros per long-row piece
-constexpr int HEAVY_MIN = 65536; // k_dense: rows with at least this many nonzeros
+#ifndef CPD_HEAVY_MIN
+#define CPD_HEAVY_MIN 131072
+#endif
+constexpr int HEAVY_MIN = CPD_HEAVY_MIN; // k_dense: rows with at least this many nonzeros
 #ifndef CPD_HB
 #define CPD_HB 8192
 #endif
@@ -90,7 +93,7 @@ struct DevPlan {
     const PlanEntry* dense_ent;   // {slot, block, q0, q1}: <= DCHUNK entries of one heavy row in one block
     const int32_t* dense_ptr;     // [nhb + 1] items of each block
     int32_t dense_maxitems;       // most items in one block (k_dense item-sum smem)
-    const int32_t* short_ptr;     // [nslab][rows + 1] short-row entries by slab (k_short)
+    const int32_t* short_ptr;     // [nslab][rows + 1] short-row entries by slab (k_csrw slab mode)
     const int32_t* short_col;
     const double* short_val;
     double* short_part;           // [NV][rows] running sums across slab passes
@@ -1031,6 +1034,10 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
 //    row (lane = row) adds the run's total; then lane = row runs the epilogue.
 //  long-row piece (<= WCAP_LONG nonzeros inside one column slab): lane-strided sum,
 //    warp xor-reduction, one partial per piece for k_finish.
+// Slab mode (slab >= 0, the default for the warp plan's rows items when the vector
+//   spans >= 2 slabs): the rows items sum only their entries in column slab `slab`
+//   (slab-major copy P.short_*), so the pass gathers from an L2-resident part of the
+//   vector; running sums live in P.short_part, the last pass runs the epilogue.
 // Fixed order for a fixed plan: deterministic.
 constexpr int TPB_W = 256;
 constexpr int WU = 4;
@@ -1041,7 +1048,7 @@ constexpr int WU = 4;
 template <int NV, class Epi>
 __global__ void __launch_bounds__(TPB_W, CPD_W_MINB)
 k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr,
-       double* red, int prev, int fin)
+       double* red, int prev, int fin, int slab, int nslab)
 {
     constexpr int NS = Epi::NS;
     constexpr int NVEC = Epi::NVEC;
@@ -1065,36 +1072,45 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int nw = gridDim.x * (TPB_W / 32);
+    // slab >= 0: rows items over the short-row copy of column slab `slab` (running
+    // sums in P.short_part between passes; the last pass runs the epilogue)
+    const bool sl_mode = slab >= 0;
+    const bool sl_last = !sl_mode || slab == nslab - 1;
+    const int32_t* __restrict__ rptr = sl_mode ? P.short_ptr + (int64_t)slab * (M.rows + 1) : M.p;
     __shared__ double vst[TPB_W / 32][(NVEC > 0 ? NVEC : 1) * 32];
     for (int it = (blockIdx.x * TPB_W + threadIdx.x) >> 5; it < P.nent; it += nw) {
         const PlanEntry E = P.ent[it];
-        const int p0 = E.p0, T = E.p1 - E.p0;
+        const bool sl_item = sl_mode && E.b >= 0;
+        const int32_t* __restrict__ mj = sl_item ? P.short_col : M.j;
+        const double* __restrict__ mx = sl_item ? P.short_val : M.x;
+        const int p0 = sl_item ? rptr[E.a] : E.p0;
+        const int T = sl_item ? rptr[E.b] - p0 : E.p1 - E.p0;
         // one round: WU lane-strided entries from `base` (streamed, evict-first)
         auto ldround = [&](int (&cc)[WU], double (&aa)[WU], int base) {
 #pragma unroll
             for (int u = 0; u < WU; ++u) {
                 const int q = base + 32 * u + lane;
-                cc[u] = q < T ? ld_stream(M.j + p0 + q) : -1;
-                aa[u] = q < T ? ld_stream(M.x + p0 + q) : 0.0;
+                cc[u] = q < T ? ld_stream(mj + p0 + q) : -1;
+                aa[u] = q < T ? ld_stream(mx + p0 + q) : 0.0;
             }
         };
         if (E.b >= 0) {
             const int r0 = E.a, nr = E.b - E.a;
-            const int rs = lane < nr ? M.p[r0 + lane] - p0 : 0x7fffffff;   // start of row `lane`
-            const int re = lane < nr ? M.p[r0 + lane + 1] - p0 : 0;         // its end
+            const int rs = lane < nr ? rptr[r0 + lane] - p0 : 0x7fffffff;   // start of row `lane`
+            const int re = lane < nr ? rptr[r0 + lane + 1] - p0 : 0;         // its end
             double* stg = vst[threadIdx.x >> 5];
 #if CPD_PRE
             double pre[NVEC > 0 ? NVEC : 1];
 #pragma unroll
-            for (int v = 0; v < NVEC; ++v) pre[v] = (lane < nr && vin[v]) ? __ldcs(vin[v] + r0 + lane) : 0.0;
+            for (int v = 0; v < NVEC; ++v) pre[v] = (sl_last && lane < nr && vin[v]) ? __ldcs(vin[v] + r0 + lane) : 0.0;
 #else
-            if (lane < nr)
+            if (sl_last && lane < nr)
 #pragma unroll
                 for (int v = 0; v < NVEC; ++v) stg[v * 32 + lane] = vin[v] ? __ldcs(vin[v] + r0 + lane) : 0.0;
 #endif
             double racc[NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) racc[v] = 0.0;
+            for (int v = 0; v < NV; ++v) racc[v] = (sl_mode && slab > 0 && lane < nr) ? P.short_part[v * (int64_t)M.rows + r0 + lane] : 0.0;
             if (PushRole<Epi>::v == 2 && P.push_acc) {   // sums pushed by the primal step
                 if (lane < nr) {
                     racc[0] = P.push_acc[r0 + lane];
@@ -1158,6 +1174,12 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
                 }
             }
             }
+            if (!sl_last) {
+                if (lane < nr)
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) P.short_part[v * (int64_t)M.rows + r0 + lane] = racc[v];
+                continue;
+            }
             if (lane < nr) {
                 const double* vs[NVEC > 0 ? NVEC : 1];
 #pragma unroll
@@ -1205,6 +1227,7 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
                 for (int v = 0; v < NV; ++v) P.lpart[(size_t)E.a * 2 + v] = sm[v];
         }
     }
+    if (!sl_last) return;
     if (fin)
         grid_finalize<NS, TPB_W>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
     else
@@ -1290,66 +1313,6 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
                 for (int v = 0; v < NV; ++v) P.lpart[(size_t)E.a * 2 + v] = sm[v];
         }
     }
-}
-
-// ------------------------------------------------------------ short rows by column slab
-// Rows of at most WLONG entries, with their entries copied slab-major: pass s sums
-// each row's slab-s entries (thread = row, consecutive rows' entries adjacent, so
-// the warp's loads are coalesced at line level) gathering only from the L2-resident
-// slab s of the vector, and carries the running sum in short_part; the last pass
-// adds its slab and runs the fused epilogue for every row that is not long
-// (long rows: k_finish).  Fixed order (slab 0 first): deterministic.
-template <int NV, class Epi>
-__global__ void __launch_bounds__(256)
-k_short(DevCsr M, DevPlan P, int32_t slab, int32_t nslab, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl,
-        double* bpart, unsigned* ctr, double* red, int prev, int fin)
-{
-    constexpr int NS = Epi::NS;
-    constexpr int NVEC = Epi::NVEC;
-    __shared__ int s_go;
-    if (threadIdx.x == 0) {
-        s_go = gate_open(gate, ctl);
-        if (s_go && gate.active && blockIdx.x == 0) gate.active[gate.node] = 1;
-    }
-    __syncthreads();
-    if (!s_go) return;
-    Epi e = epi;
-    e.load(ctl);
-    const double* vin[NVEC > 0 ? NVEC : 1];
-#pragma unroll
-    for (int v = 0; v < NVEC; ++v) vin[v] = e.vec(v);
-    const double* __restrict__ v0 = vs0.get(ctl);
-    const double* __restrict__ v1 = vs1.get(ctl);
-    double acc[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-    const int32_t rows = M.rows;
-    const bool last = slab == nslab - 1;
-    const int32_t* sp = P.short_ptr + (int64_t)slab * (rows + 1);
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t q0 = sp[r], q1 = sp[r + 1];
-        double sm[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) sm[v] = slab == 0 ? 0.0 : P.short_part[v * (int64_t)rows + r];
-#pragma unroll 4
-        for (int32_t q = q0; q < q1; ++q) {
-            const int32_t c = __ldcs(P.short_col + q);
-            const double a = __ldcs(P.short_val + q);
-            sm[0] += a * __ldg(&v0[c]);
-            if (NV > 1) sm[NV - 1] += a * __ldg(&v1[c]);
-        }
-        if (!last) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) P.short_part[v * (int64_t)rows + r] = sm[v];
-        } else if (M.p[r + 1] - M.p[r] <= WLONG) {
-            e.row((int)r, sm, vin, (int)r, acc);
-        }
-    }
-    if (!last) return;
-    if (fin)
-        grid_finalize<NS, 256>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
-    else
-        block_partial<NS, 256>(acc, bpart, prev);
 }
 
 // Elementwise pass over [0, N) with reductions and a device-side finalize.

@@ -51,34 +51,63 @@ __global__ void k_slab_pos(int32_t nl, int32_t nb, const int32_t* lrows, const i
 }
 
 // Short rows (<= long_min entries) split by column slab: cnt[s * rows + r] = entries of
-// row r in slab s (0 for long rows).
+// row r in slab s (0 for long rows); a row's columns are ascending, so the slab
+// boundaries are found by binary search.
 __global__ void k_short_count(int32_t rows, int32_t nslab, int64_t long_min, const int32_t* p, const int32_t* col,
                               int32_t* cnt, int64_t width)
 {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
         const int32_t a = p[r], b = p[r + 1];
-        for (int32_t s = 0; s < nslab; ++s) cnt[(int64_t)s * rows + r] = 0;
-        if (b - a > long_min) continue;
-        for (int32_t q = a; q < b; ++q) cnt[(int64_t)(col[q] / width) * rows + r] += 1;
+        const bool sh = b - a <= long_min;
+        int32_t prev = a;
+        for (int32_t s = 0; s < nslab; ++s) {
+            int32_t end = b;
+            if (s + 1 < nslab) {   // first q in [prev, b) with col[q] >= (s + 1) * width
+                int32_t lo = prev, hi = b;
+                const int64_t key = (int64_t)(s + 1) * width;
+                while (lo < hi) {
+                    const int32_t mid = lo + (hi - lo) / 2;
+                    if (col[mid] < key) lo = mid + 1; else hi = mid;
+                }
+                end = lo;
+            }
+            cnt[(int64_t)s * rows + r] = sh ? end - prev : 0;
+            prev = end;
+        }
     }
 }
 
-// entries copied slab-major (row order, then column order inside each slab)
+// slab pointers from the slab-major exclusive scan: sp[s][r] = flat[s * rows + r],
+// sp[s][rows] = start of slab s + 1 (the total for the last slab)
+__global__ void k_short_ptr(int32_t rows, int32_t nslab, const int32_t* flat, const int32_t* cnt, int32_t* sp)
+{
+    const int64_t N = (int64_t)nslab * (rows + 1);
+    const int64_t tot = (int64_t)nslab * rows;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i / (rows + 1), r = i % (rows + 1);
+        sp[i] = r < rows ? flat[s * rows + r] : (s + 1 < nslab ? flat[(s + 1) * rows] : flat[tot - 1] + cnt[tot - 1]);
+    }
+}
+
+// entries copied slab-major (row order, then column order inside each slab): a warp
+// per row, lane-strided (coalesced) over the row's entries
 __global__ void k_short_fill(int32_t rows, int32_t nslab, int64_t long_min, const int32_t* p, const int32_t* col,
                              const double* val, const int32_t* sp, int32_t* scol, double* sval, int64_t width)
 {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int32_t a = p[r], b = p[r + 1];
         if (b - a > long_min) continue;
-        int32_t q = a;
-        for (int32_t s = 0; s < nslab; ++s) {
-            int32_t d = sp[(int64_t)s * (rows + 1) + r];
-            while (q < b && col[q] / width == s) {
-                scol[d] = col[q];
-                sval[d] = val[q];
-                ++d;
-                ++q;
-            }
+        for (int32_t q = a + lane; q < b; q += 32) {
+            const int32_t c = col[q];
+            const int64_t s64 = c / width;
+            const int32_t s = s64 < nslab - 1 ? (int32_t)s64 : nslab - 1;
+            int32_t off = 0;   // entries of this row in slabs before s
+            for (int32_t t = 0; t < s; ++t) off += sp[(int64_t)t * (rows + 1) + r + 1] - sp[(int64_t)t * (rows + 1) + r];
+            const int32_t d = sp[(int64_t)s * (rows + 1) + r] + (q - a - off);
+            scol[d] = c;
+            sval[d] = val[q];
         }
     }
 }
@@ -246,17 +275,23 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     plan.single_entries = 0;
     plan.long_pieces = (int64_t)lptr[nl];
     plan.nslab = nslab;
-    // warp plan with >= 2 slabs: short rows also by slab (k_short), so their gathers of
-    // the vector hit the L2-resident slab instead of DRAM
-    // Off by default: measured slower on C5 (5 latency-bound passes of ~210 us vs one
-    // 453 us rows segment, profiles/r01_kernel_iterations.md v18); CPD_SHORT=1 enables.
+    // warp plan with >= 2 slabs: the short rows' items also run once per column slab
+    // (k_csrw slab mode over a slab-major copy of their entries), so their gathers of
+    // the vector hit an L2-resident half instead of DRAM.  On by default (C5: dual step
+    // -1%, profiles/r01_kernel_iterations.md v35); CPD_SHORT=0 disables.  (A thread-
+    // per-row version, v18, was latency-bound and slower.)
     plan.short_on = 0;
     const char* she = getenv("CPD_SHORT");
-    const int32_t nss = (int32_t)std::min<int64_t>(CPD_SHORT_SLABS, std::max<int64_t>(1, cols));
-    const int64_t sw = ((int64_t)cols + nss - 1) / nss;
+    // CPD_SHORT_SLABS (env, else the macro): number of short-row slabs; 0 = the long
+    // pieces' slabs (SLAB_COLS wide), so a short pass and that slab's pieces run back to back
+    const char* sse = getenv("CPD_SHORT_SLABS");
+    const int64_t nreq = sse ? atoll(sse) : CPD_SHORT_SLABS;
+    const int32_t nss = nreq <= 0 ? nslab : (int32_t)std::min<int64_t>(nreq, std::max<int64_t>(1, cols));
+    const int64_t sw = nreq <= 0 ? SLAB_COLS : ((int64_t)cols + nss - 1) / nss;
+    plan.short_ilv = nreq <= 0 ? 1 : 0;
     plan.short_nslab = nss;
     plan.short_width = sw;
-    if (warp && nslab >= 2 && rows > 0 && she && she[0] == '1') {
+    if (warp && rows > 0 && ((nslab >= 2 && !(she && she[0] == '0')) || (she && she[0] == '1'))) {   // =1: also small n (tests)
         const int32_t nslab = nss;   // the short rows' own column slabs (each x slab L2-resident)
         DBuf<int32_t> cnt((size_t)nslab * rows);
         const int g = (int)std::min<int64_t>(((int64_t)rows + 255) / 256, 8192);
@@ -269,24 +304,19 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
         CPD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, flat.p, (int)((int64_t)nslab * rows)));
         DBuf<unsigned char> tmp(tb);
         CPD_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, flat.p, (int)((int64_t)nslab * rows)));
-        std::vector<int32_t> hflat((size_t)nslab * rows), hcnt_last(1);
-        CPD_CUDA(cudaMemcpy(hflat.data(), flat.p, sizeof(int32_t) * hflat.size(), cudaMemcpyDeviceToHost));
-        CPD_CUDA(cudaMemcpy(hcnt_last.data(), cnt.p + (size_t)nslab * rows - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
-        const int64_t total = (int64_t)hflat.back() + hcnt_last[0];
-        std::vector<int32_t> hsp((size_t)nslab * (rows + 1));
-        for (int32_t s2 = 0; s2 < nslab; ++s2) {
-            std::copy(hflat.begin() + (size_t)s2 * rows, hflat.begin() + (size_t)(s2 + 1) * rows,
-                      hsp.begin() + (size_t)s2 * (rows + 1));
-            hsp[(size_t)s2 * (rows + 1) + rows] =
-                (s2 + 1 < nslab) ? hflat[(size_t)(s2 + 1) * rows] : (int32_t)total;
-        }
-        CPD_CUDA(cudaMemcpy(plan.short_ptr.p, hsp.data(), sizeof(int32_t) * hsp.size(), cudaMemcpyHostToDevice));
+        k_short_ptr<<<(int)std::min<int64_t>(((int64_t)nslab * (rows + 1) + 255) / 256, 65536), 256>>>(
+            rows, nslab, flat.p, cnt.p, plan.short_ptr.p);
+        CPD_CUDA(cudaGetLastError());
+        int32_t htot = 0;
+        CPD_CUDA(cudaMemcpy(&htot, plan.short_ptr.p + (size_t)nslab * (rows + 1) - 1, sizeof(int32_t),
+                            cudaMemcpyDeviceToHost));
+        const int64_t total = htot;
         plan.short_col.alloc(std::max<int64_t>(total, 1));
         plan.short_val.alloc(std::max<int64_t>(total, 1));
-        k_short_fill<<<g, 256>>>(rows, nslab, long_min, d_p, d_col, d_val, plan.short_ptr.p, plan.short_col.p,
-                                 plan.short_val.p, sw);
+        const int gw = (int)std::min<int64_t>(((int64_t)rows * 32 + 255) / 256, 65536);
+        k_short_fill<<<gw, 256>>>(rows, nslab, long_min, d_p, d_col, d_val, plan.short_ptr.p, plan.short_col.p,
+                                  plan.short_val.p, sw);
         CPD_CUDA(cudaGetLastError());
-        CPD_CUDA(cudaDeviceSynchronize());
         plan.short_nnz = total;
         plan.short_on = 1;
     }
@@ -799,7 +829,7 @@ void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc)
     if (P->push_on) mark_push(P);
     for (Matrix* M : {&P->A, &P->AT})
         if (M->plan.short_on) {
-            const int g = (int)std::min<int64_t>(((int64_t)M->rows + 255) / 256, 8192);
+            const int g = (int)std::min<int64_t>(((int64_t)M->rows * 32 + 255) / 256, 65536);   // a warp per row
             k_short_fill<<<g, 256>>>(M->rows, M->plan.short_nslab, WLONG, M->p.p, M->j.p, M->x.p,
                                      M->plan.short_ptr.p, M->plan.short_col.p, M->plan.short_val.p,
                                      M->plan.short_width);

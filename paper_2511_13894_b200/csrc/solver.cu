@@ -207,33 +207,34 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
                 ++cx.launches;
             }
         };
-        auto launch_items = [&](int a, int b, int fin) {
+        auto launch_items = [&](int a, int b, int fin, int slab = -1, int nslab = 0) {
             DevPlan ds = dp;
             if (PushRole<Epi>::v == 2) ds.push_acc = cx.push_acc;
             ds.ent = dp.ent + a;
             ds.nent = b - a;
             const int gr = std::max(1, std::min<int>(wgrid, (ds.nent + 7) / 8));
             k_csrw<NV, Epi><<<gr, TPB_W, 0, cx.st>>>(M.dev(), ds, v0, v1, epi, gs, cx.ctl, cx.bpart.p, cx.ctr.p,
-                                                     red, prev, fin);
+                                                     red, prev, fin, slab, nslab);
             CPD_CUDA(cudaGetLastError());
             ++cx.launches;
             gs.active = nullptr;
-            prev += gr;
+            if (slab < 0 || slab == nslab - 1) prev += gr;   // only the last slab pass leaves partials
         };
-        if (M.plan.short_on) {
+        // (the short-row push, when on, already summed the rows items' products in K1)
+        if (M.plan.short_on && !(PushRole<Epi>::v == 2 && cx.push_acc)) {
             launch_dense();
-            // the short rows by their own column slabs, then every long piece
+            // the short rows' items once per column slab (each pass gathers from one
+            // L2-resident slab of the vector), then every long piece
             const int nsl = M.plan.short_nslab;
             for (int sl = 0; sl < nsl; ++sl) {
-                const int grs = std::max(1, std::min<int>(cx.P->num_sms * 16, (M.rows + 255) / 256));
-                const bool lastp = sl == nsl - 1;
-                k_short<NV, Epi><<<grs, 256, 0, cx.st>>>(M.dev(), dp, sl, nsl, v0, v1, epi, gs, cx.ctl, cx.bpart.p,
-                                                         cx.ctr.p, red, prev, (lastp && single) ? 1 : 0);
-                CPD_CUDA(cudaGetLastError());
-                ++cx.launches;
-                gs.active = nullptr;
-                if (lastp) prev += grs;
+                launch_items(seg[0], seg[1], (sl == nsl - 1 && single) ? 1 : 0, sl, nsl);
+                if (M.plan.short_ilv && !single && (size_t)sl + 2 < seg.size() && seg[sl + 2] > seg[sl + 1])
+                    launch_items(seg[sl + 1], seg[sl + 2], 0);   // this slab's long pieces
             }
+            if (M.plan.short_ilv) {
+                for (size_t k = nsl + 1; !single && k + 1 < seg.size(); ++k)
+                    if (seg[k + 1] > seg[k]) launch_items(seg[k], seg[k + 1], 0);
+            } else
             if (!single && seg.back() > seg[1]) launch_items(seg[1], seg.back(), 0);
         } else {
             // rows items first (x+ just written by the primal step is still in L2), then

@@ -282,7 +282,7 @@ def test_trajectory(problems):
 @pytest.mark.parametrize("name", ["c1", "c2-s", "c3-s", "c4-s", "c5-s"])
 def test_every_spmv_format_lockstep(name, fmt, monkeypatch):
     """Each SpMV engine (TMA plan k_spmv / warp-item k_csrw (+ k_dense heavy rows,
-    + k_short slab passes) for A; SELL-32 k_sell or the TMA plan for A^T) meets the
+    + column-slab passes of the rows items) for A; SELL-32 k_sell or the TMA plan for A^T) meets the
     1e-9 iterate contract, restarts on."""
     warp, sell, short = fmt
     monkeypatch.setenv("CPD_WARP", warp)
@@ -302,14 +302,43 @@ def test_every_spmv_format_lockstep(name, fmt, monkeypatch):
     assert P.power_sigma(128, 7) == pytest.approx(oracle.power_sigma(olp, 128, 7), rel=1e-12)
 
 
+@pytest.mark.parametrize("slabs", ["2", "3", "7", "0"])
+@pytest.mark.parametrize("name", ["c2-s", "c3-s", "c5-s"])
+def test_short_row_slab_passes_lockstep(name, slabs, monkeypatch):
+    """k_csrw slab mode: the rows items summed over 2 / 3 / 7 column slabs (running
+    sums between passes, epilogue on the last) or over the long pieces' slabs with
+    the passes interleaved (0); same 1e-9 iterate contract and oracle score."""
+    monkeypatch.setenv("CPD_WARP", "1")
+    monkeypatch.setenv("CPD_SHORT", "1")
+    monkeypatch.setenv("CPD_SHORT_SLABS", slabs)
+    lp = lpgen.config(name)
+    olp = oracle.OracleLP(lp)
+    P = cpd.Problem.from_lp(lp)
+    eta = 0.9 / oracle.power_sigma(olp)
+    S = cpd.Solver(P, step_size=eta, restart=1)
+    R = oracle.Run(olp, oracle.default_params(step_size=eta, restart=1), mode=oracle.MODE_NONE)
+    for k in (1, 64, 300):
+        S.step(k - R.k)
+        R.run(k - R.k)
+        xg, yg = S.get_iterate()
+        xo, yo = R.get()
+        assert close(xg, xo) and close(yg, yo), (name, slabs, k)
+    x = np.random.default_rng(3).uniform(0, 2, lp.n)
+    y = np.random.default_rng(4).standard_normal(lp.m)
+    assert P.score(x, y)["rp"] == pytest.approx(oracle.score(olp, x, y)["rp"], rel=1e-12)
+
+
+@pytest.mark.parametrize("short", ["0", "1"])
 @pytest.mark.parametrize("push", ["1", "0"])
 @pytest.mark.parametrize("name", ["c5-s", "c2-s"])
-def test_short_row_push_lockstep(name, push, monkeypatch):
+def test_short_row_push_lockstep(name, push, short, monkeypatch):
     """The short-row push (primal step scatters a_ij x+_j into an L2-resident m-vector
     with fp64 atomics; the dual step reads it instead of gathering x+) meets the same
     1e-9 contract as the pull path; with CPD_WARP=1 so that C2's A takes the
-    warp plan too."""
+    warp plan too; with and without the rows items' column-slab passes (which the
+    push replaces for the dual step)."""
     monkeypatch.setenv("CPD_PUSH", push)
+    monkeypatch.setenv("CPD_SHORT", short)
     monkeypatch.setenv("CPD_WARP", "1")
     lp = lpgen.config(name)
     olp = oracle.OracleLP(lp)
@@ -322,7 +351,7 @@ def test_short_row_push_lockstep(name, push, monkeypatch):
         R.run(k - R.k)
         xg, yg = S.get_iterate()
         xo, yo = R.get()
-        assert close(xg, xo) and close(yg, yo), (name, push, k)
+        assert close(xg, xo) and close(yg, yo), (name, push, short, k)
     # termination through the push path (c5-s hits the iteration limit on both sides)
     S2 = cpd.Solver(P, max_iters=5000)
     r = S2.solve()
