@@ -79,6 +79,7 @@ struct Plan {
     int64_t short_width = 0;
     int64_t short_nnz = 0;
     DBuf<int32_t> short_ptr, short_col;
+    DBuf<PlanEntry> short_ent;   // [nslab][seg[1]] rows items with p0/p1 in the slab-major copy
     DBuf<double> short_val;
     int64_t rows_entries = 0, single_entries = 0, long_pieces = 0;
     int32_t nslab = 1;

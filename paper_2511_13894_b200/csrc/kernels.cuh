@@ -1036,7 +1036,8 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
 //    warp xor-reduction, one partial per piece for k_finish.
 // Slab mode (slab >= 0, the default for the warp plan's rows items when the vector
 //   spans >= 2 slabs): the rows items sum only their entries in column slab `slab`
-//   (slab-major copy P.short_*), so the pass gathers from an L2-resident part of the
+//   (slab-major copy P.short_*, items re-based per slab at create), so the pass
+//   gathers from an L2-resident part of the
 //   vector; running sums live in P.short_part, the last pass runs the epilogue.
 // Fixed order for a fixed plan: deterministic.
 constexpr int TPB_W = 256;
@@ -1083,8 +1084,7 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
         const bool sl_item = sl_mode && E.b >= 0;
         const int32_t* __restrict__ mj = sl_item ? P.short_col : M.j;
         const double* __restrict__ mx = sl_item ? P.short_val : M.x;
-        const int p0 = sl_item ? rptr[E.a] : E.p0;
-        const int T = sl_item ? rptr[E.b] - p0 : E.p1 - E.p0;
+        const int p0 = E.p0, T = E.p1 - E.p0;   // (slab mode: P.ent = the slab's own items)
         // one round: WU lane-strided entries from `base` (streamed, evict-first)
         auto ldround = [&](int (&cc)[WU], double (&aa)[WU], int base) {
 #pragma unroll

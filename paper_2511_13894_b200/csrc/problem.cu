@@ -89,6 +89,20 @@ __global__ void k_short_ptr(int32_t rows, int32_t nslab, const int32_t* flat, co
     }
 }
 
+// the rows items re-based per slab: {a, b, sp[s][a], sp[s][b]} (k_csrw slab mode
+// reads the item's entry range directly, one dependent load less per item)
+__global__ void k_short_ents(int32_t ni, int32_t nslab, int32_t rows, const PlanEntry* ent, const int32_t* sp,
+                             PlanEntry* out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)nslab * ni;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i / ni;
+        const PlanEntry E = ent[i % ni];
+        const int32_t* p = sp + s * (rows + 1);
+        out[i] = PlanEntry{E.a, E.b, p[E.a], p[E.b]};
+    }
+}
+
 // entries copied slab-major (row order, then column order inside each slab): a warp
 // per row, lane-strided (coalesced) over the row's entries
 __global__ void k_short_fill(int32_t rows, int32_t nslab, int64_t long_min, const int32_t* p, const int32_t* col,
@@ -322,6 +336,14 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     }
     plan.ent.alloc(std::max<size_t>(ent.size(), 1));
     CPD_CUDA(cudaMemcpy(plan.ent.p, ent.data(), sizeof(PlanEntry) * ent.size(), cudaMemcpyHostToDevice));
+    if (plan.short_on && plan.seg[1] > 0) {
+        const int32_t ni = plan.seg[1];
+        plan.short_ent.alloc((size_t)plan.short_nslab * ni);
+        const int64_t tot = (int64_t)plan.short_nslab * ni;
+        k_short_ents<<<(int)std::min<int64_t>((tot + 255) / 256, 65536), 256>>>(ni, plan.short_nslab, rows, plan.ent.p,
+                                                                             plan.short_ptr.p, plan.short_ent.p);
+        CPD_CUDA(cudaGetLastError());
+    }
     plan.long_row.alloc(std::max(nl, 1));
     plan.long_ptr.alloc(nl + 1);
     // k_finish order: long rows with > FIN_SPLIT partials first (a CTA each), then the

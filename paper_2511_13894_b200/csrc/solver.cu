@@ -210,7 +210,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         auto launch_items = [&](int a, int b, int fin, int slab = -1, int nslab = 0) {
             DevPlan ds = dp;
             if (PushRole<Epi>::v == 2) ds.push_acc = cx.push_acc;
-            ds.ent = dp.ent + a;
+            ds.ent = (slab >= 0 ? M.plan.short_ent.p + (size_t)slab * M.plan.seg[1] : dp.ent) + a;
             ds.nent = b - a;
             const int gr = std::max(1, std::min<int>(wgrid, (ds.nent + 7) / 8));
             k_csrw<NV, Epi><<<gr, TPB_W, 0, cx.st>>>(M.dev(), ds, v0, v1, epi, gs, cx.ctl, cx.bpart.p, cx.ctr.p,
