@@ -1038,7 +1038,8 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
 //   spans >= 2 slabs): the rows items sum only their entries in column slab `slab`
 //   (slab-major copy P.short_*, items re-based per slab at create), so the pass
 //   gathers from an L2-resident part of the
-//   vector; running sums live in P.short_part, the last pass runs the epilogue.
+//   vector; running sums live in P.short_part, the last pass (spass bit 1) runs the
+//   epilogue, the first (bit 0) starts the sums.
 // Fixed order for a fixed plan: deterministic.
 constexpr int TPB_W = 256;
 constexpr int WU = 4;
@@ -1049,7 +1050,7 @@ constexpr int WU = 4;
 template <int NV, class Epi>
 __global__ void __launch_bounds__(TPB_W, CPD_W_MINB)
 k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr,
-       double* red, int prev, int fin, int slab, int nslab)
+       double* red, int prev, int fin, int slab, int spass)
 {
     constexpr int NS = Epi::NS;
     constexpr int NVEC = Epi::NVEC;
@@ -1076,7 +1077,7 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
     // slab >= 0: rows items over the short-row copy of column slab `slab` (running
     // sums in P.short_part between passes; the last pass runs the epilogue)
     const bool sl_mode = slab >= 0;
-    const bool sl_last = !sl_mode || slab == nslab - 1;
+    const bool sl_last = !sl_mode || (spass & 2);   // spass: bit 0 first pass, bit 1 last pass
     const int32_t* __restrict__ rptr = sl_mode ? P.short_ptr + (int64_t)slab * (M.rows + 1) : M.p;
     __shared__ double vst[TPB_W / 32][(NVEC > 0 ? NVEC : 1) * 32];
     for (int it = (blockIdx.x * TPB_W + threadIdx.x) >> 5; it < P.nent; it += nw) {
@@ -1110,7 +1111,7 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
 #endif
             double racc[NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) racc[v] = (sl_mode && slab > 0 && lane < nr) ? P.short_part[v * (int64_t)M.rows + r0 + lane] : 0.0;
+            for (int v = 0; v < NV; ++v) racc[v] = (sl_mode && !(spass & 1) && lane < nr) ? P.short_part[v * (int64_t)M.rows + r0 + lane] : 0.0;
             if (PushRole<Epi>::v == 2 && P.push_acc) {   // sums pushed by the primal step
                 if (lane < nr) {
                     racc[0] = P.push_acc[r0 + lane];

@@ -207,18 +207,18 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
                 ++cx.launches;
             }
         };
-        auto launch_items = [&](int a, int b, int fin, int slab = -1, int nslab = 0) {
+        auto launch_items = [&](int a, int b, int fin, int slab = -1, int spass = 0) {
             DevPlan ds = dp;
             if (PushRole<Epi>::v == 2) ds.push_acc = cx.push_acc;
             ds.ent = (slab >= 0 ? M.plan.short_ent.p + (size_t)slab * M.plan.seg[1] : dp.ent) + a;
             ds.nent = b - a;
             const int gr = std::max(1, std::min<int>(wgrid, (ds.nent + 7) / 8));
             k_csrw<NV, Epi><<<gr, TPB_W, 0, cx.st>>>(M.dev(), ds, v0, v1, epi, gs, cx.ctl, cx.bpart.p, cx.ctr.p,
-                                                     red, prev, fin, slab, nslab);
+                                                     red, prev, fin, slab, spass);
             CPD_CUDA(cudaGetLastError());
             ++cx.launches;
             gs.active = nullptr;
-            if (slab < 0 || slab == nslab - 1) prev += gr;   // only the last slab pass leaves partials
+            if (slab < 0 || (spass & 2)) prev += gr;   // only the last slab pass leaves partials
         };
         // (the short-row push, when on, already summed the rows items' products in K1)
         if (M.plan.short_on && !(PushRole<Epi>::v == 2 && cx.push_acc)) {
@@ -226,8 +226,10 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
             // the short rows' items once per column slab (each pass gathers from one
             // L2-resident slab of the vector), then every long piece
             const int nsl = M.plan.short_nslab;
-            for (int sl = 0; sl < nsl; ++sl) {
-                launch_items(seg[0], seg[1], (sl == nsl - 1 && single) ? 1 : 0, sl, nsl);
+            for (int i = 0; i < nsl; ++i) {
+                const int sl = i;   // (reverse order, or the dense blocks after the passes: no different, v40)
+                const int sp = (i == 0 ? 1 : 0) | (i == nsl - 1 ? 2 : 0);
+                launch_items(seg[0], seg[1], (i == nsl - 1 && single) ? 1 : 0, sl, sp);
                 if (M.plan.short_ilv && !single && (size_t)sl + 2 < seg.size() && seg[sl + 2] > seg[sl + 1])
                     launch_items(seg[sl + 1], seg[sl + 2], 0);   // this slab's long pieces
             }
