@@ -109,6 +109,8 @@ def lib():
             L.orc_get_omega.argtypes = [P]
             L.orc_get_k.restype = C.c_int64
             L.orc_get_k.argtypes = [P]
+            L.orc_get_restart_state.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
             L.orc_reduced_costs.argtypes = [C.POINTER(LPStruct), P, P, P]
             L.orc_corner_model.argtypes = [C.c_int32, P, P, P, P, C.c_double, C.c_double,
                                            C.c_uint64, P, P, P, C.POINTER(C.c_int64),
@@ -247,6 +249,12 @@ class Run:
     @property
     def omega(self):
         return float(lib().orc_get_omega(self.h))
+
+    def restart_state(self) -> dict:
+        """S_r, S_prev, t (iterations since the last restart) and the restart count."""
+        sr, sp, t, nr = C.c_double(), C.c_double(), C.c_int64(), C.c_int64()
+        lib().orc_get_restart_state(self.h, C.byref(sr), C.byref(sp), C.byref(t), C.byref(nr))
+        return dict(S_r=sr.value, S_prev=sp.value, t=t.value, restarts=nr.value)
 
     def get(self):
         x = np.zeros(self.olp.n)

@@ -370,6 +370,18 @@ double orc_get_eta(const orc_state *s) { return s->eta; }
 double orc_get_omega(const orc_state *s) { return s->omega; }
 int64_t orc_get_k(const orc_state *s) { return s->k; }
 
+/* Restart bookkeeping of a run (read-only test access for the restart pins,
+ * tests/golden/restart_2x2.json): reference score S_r, previous candidate score
+ * S_prev, iterations since the last restart t, and the restart count. */
+void orc_get_restart_state(const orc_state *s, double *S_r, double *S_prev, int64_t *t,
+                           int64_t *restarts)
+{
+    *S_r = s->S_r;
+    *S_prev = s->S_prev;
+    *t = s->t;
+    *restarts = s->restarts;
+}
+
 /* Mark a run as the scaled image of `orig` (objective oc, bounds ol/ou in original
  * space, x = sc x^, y = sr y^): termination, restart scores and the primal-only
  * residual are then evaluated on the original LP; everything else (steps, primal
