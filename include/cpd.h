@@ -52,7 +52,7 @@ enum cpd_error {
     CPD_E_NONFINITE = -5,  /* NaN/Inf in A, b or c (only bounds may be infinite) */
     CPD_E_CUDA = -6,       /* CUDA runtime error (message has the CUDA error string) */
     CPD_E_NCCL = -7,       /* NCCL error */
-    CPD_E_STATE = -8,      /* call not valid in the handle's state (e.g. corner push before a solve) */
+    CPD_E_STATE = -8,      /* call not valid in the handle's state (e.g. scale while a solver is alive) */
     CPD_E_NOMEM = -9       /* device allocation failed */
 };
 
@@ -93,6 +93,12 @@ int cpd_problem_create(int32_t m, int32_t n, int64_t nnz,
 int cpd_problem_destroy(cpd_problem *p);
 /* m, n, nnz, number of long (split) rows in each layout's SpMV plan. */
 int cpd_problem_info(const cpd_problem *p, int64_t info[8]);
+/* Which SpMV engine paths the problem's plans use, for tests and
+ * diagnostics: out[12] = {A warp plan (k_csrw) 1/0, A heavy rows (k_dense), A dense
+ * column blocks, A column slabs of the long pieces, A short-row slab passes
+ * (0 = off), A long rows, A long pieces, A rows items, A^T SELL-32 1/0, hot rows
+ * (renumbered), A TMA plan entries (k_spmv), reserved 0}. */
+int cpd_problem_plan_info(const cpd_problem *p, int64_t out[12]);
 
 /* Solver parameters (every constant of the R-PDHG reading, §8(c)). */
 typedef struct {
@@ -212,8 +218,9 @@ int cpd_kernel_bytes(const cpd_solver *s, const char *name, double *bytes);
  * The dual step is projected onto y_i >= 0 ('>='), y_i <= 0 ('<='); the primal
  * residual counts violations only; the corner model turns an inequality row whose
  * slack has a non-trivial reduced cost (|y*_i| > eps_abs) into an equality
- * (cpd_stats.rows_eq counts them).  Call before creating solvers.  CPD_E_ARG on a
- * value outside {0, 1, 2}. */
+ * (cpd_stats.rows_eq counts them).  Call before creating solvers: CPD_E_STATE
+ * while a solver created on `p` is alive (its captured graphs hold the problem's
+ * device pointers).  CPD_E_ARG on a value outside {0, 1, 2}. */
 int cpd_problem_set_senses(cpd_problem *p, const int8_t *sense, int32_t mem);
 
 /* ------------------------------------------------------------------ preconditioning
@@ -227,7 +234,7 @@ int cpd_problem_set_senses(cpd_problem *p, const int8_t *sense, int32_t mem);
  * scores, the steering stop and all statistics are those of the ORIGINAL LP
  * (P:119-131), and every iterate in or out of the ABI is original-space.
  * Call once, before creating solvers; single-GPU problems only (CPD_E_ARG otherwise,
- * CPD_E_STATE if already scaled). */
+ * CPD_E_STATE if already scaled or while a solver created on `p` is alive). */
 int cpd_problem_scale(cpd_problem *p, int32_t ruiz_iters, int32_t pock_chambolle);
 /* The scale vectors r[m], s[n] (host); CPD_E_STATE if the problem is not scaled. */
 int cpd_problem_get_scaling(const cpd_problem *p, double *r, double *s);

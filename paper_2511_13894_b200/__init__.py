@@ -32,7 +32,7 @@ DECLARED_SYMBOLS = [
     "cpd_get_trajectory", "cpd_power_sigma", "cpd_problem_score", "cpd_compute_stats",
     "cpd_get_kernel_times", "cpd_kernel_bytes", "cpd_solver_counters",
     "cpd_partition", "cpd_nccl_get_unique_id", "cpd_problem_create_dist", "cpd_problem_dist_info",
-    "cpd_problem_scale", "cpd_problem_get_scaling", "cpd_problem_set_senses",
+    "cpd_problem_scale", "cpd_problem_get_scaling", "cpd_problem_set_senses", "cpd_problem_plan_info",
 ]
 
 
@@ -94,6 +94,7 @@ def lib():
                                              C.POINTER(P)]),
             "cpd_problem_destroy": (C.c_int, [P]),
             "cpd_problem_info": (C.c_int, [P, P]),
+            "cpd_problem_plan_info": (C.c_int, [P, P]),
             "cpd_params_default": (None, [C.POINTER(Params)]),
             "cpd_corner_params_default": (None, [C.POINTER(CornerParams)]),
             "cpd_solver_create": (C.c_int, [P, C.POINTER(Params), C.POINTER(P)]),
@@ -135,14 +136,27 @@ def _check(rc):
     return rc
 
 
-def _ptr(a, dtype=None):
-    """(pointer, mem, keepalive) for a numpy array / torch tensor / None."""
+def _ptr(a, dtype=None, device=None):
+    """(pointer, mem, keepalive) for a numpy array / torch tensor / None.
+
+    Host arrays are converted to a contiguous copy of `dtype`.  A CUDA tensor is
+    passed by pointer, so it must already have exactly that dtype, be contiguous and
+    live on `device` (the problem's GPU): anything else raises ValueError instead of
+    being reinterpreted by the library."""
     if a is None:
         return None, HOST, None
     try:
         import torch
         if isinstance(a, torch.Tensor):
             if a.is_cuda:
+                want = {np.dtype(np.int32): torch.int32, np.dtype(np.float64): torch.float64,
+                        np.dtype(np.int8): torch.int8}.get(np.dtype(dtype)) if dtype is not None else None
+                if want is not None and a.dtype != want:
+                    raise ValueError(f"CUDA tensor has dtype {a.dtype}, the ABI expects {want}")
+                if not a.is_contiguous():
+                    raise ValueError("CUDA tensor must be contiguous")
+                if device is not None and a.device.index != int(device):
+                    raise ValueError(f"CUDA tensor is on cuda:{a.device.index}, the problem on cuda:{device}")
                 return a.data_ptr(), DEVICE, a
             a = a.numpy()
     except ImportError:
@@ -200,13 +214,13 @@ class Problem:
                 continue
             p_, j_, x_ = layout
             for a, dt in ((p_, np.int32), (j_, np.int32), (x_, np.float64)):
-                ptr, mem, k = _ptr(a, dt)
+                ptr, mem, k = _ptr(a, dt, device)
                 ptrs.append(ptr)
                 keep.append(k)
                 mems.add(mem)
             nnz = int(j_.shape[0]) if nnz is None else nnz
         for a in (b, c, lb, ub):
-            ptr, mem, k = _ptr(a, np.float64)
+            ptr, mem, k = _ptr(a, np.float64, device)
             ptrs.append(ptr)
             keep.append(k)
             if a is not None:
@@ -218,6 +232,7 @@ class Problem:
         _check(lib().cpd_problem_create(self.m, self.n, nnz, *ptrs, self.mem, device, C.byref(h)))
         self.h = h
         self.nnz = nnz
+        self.device = device
 
     @classmethod
     def from_lp(cls, lp, device=0, both=False, on_device=False):
@@ -253,6 +268,7 @@ class Problem:
         self.h = h
         self.nnz = int(lp.ATp[-1])
         self.mem = HOST
+        self.device = device
         if getattr(lp, "sense", None) is not None:
             self.set_senses(lp.sense)
         return self
@@ -287,6 +303,14 @@ class Problem:
                 "uniform_bounds")
         return dict(zip(keys, list(out)))
 
+    def plan_info(self):
+        """cpd_problem_plan_info: which SpMV engine paths the plans use."""
+        out = (C.c_int64 * 12)()
+        _check(lib().cpd_problem_plan_info(self.h, out))
+        keys = ("warp", "heavy_rows", "dense_blocks", "slabs", "short_slabs", "long_rows", "long_pieces",
+                "rows_items", "sell_AT", "hot_rows", "tma_entries")
+        return dict(zip(keys, list(out)))
+
     def power_sigma(self, iters=128, seed=7):
         s = C.c_double()
         _check(lib().cpd_power_sigma(self.h, iters, seed, C.byref(s)))
@@ -294,14 +318,14 @@ class Problem:
 
     def score(self, x, y):
         out = np.zeros(8)
-        px, mx, kx = _ptr(x, np.float64)
-        py, my, ky = _ptr(y, np.float64)
+        px, mx, kx = _ptr(x, np.float64, self.device)
+        py, my, ky = _ptr(y, np.float64, self.device)
         _check(lib().cpd_problem_score(self.h, px, py, mx, out.ctypes.data))
         return dict(zip(("rp", "rd", "pobj", "dobj", "r_p", "r_d", "r_g", "score"), out.tolist()))
 
     def stats(self, x, z=None, lhat=None, uhat=None, eps_abs=1e-6, floor=100_000):
         st = Stats()
-        args = [_ptr(a, np.float64) for a in (x, z, lhat, uhat)]
+        args = [_ptr(a, np.float64, self.device) for a in (x, z, lhat, uhat)]
         mems = {m for (p, m, _), a in zip(args, (x, z, lhat, uhat)) if a is not None}
         mem = mems.pop() if mems else HOST
         _check(lib().cpd_compute_stats(self.h, *[p for p, _, _ in args], eps_abs, floor, mem, C.byref(st)))
@@ -338,7 +362,7 @@ class Solver:
         cp = params or cpd_corner_params_default(**kw)
         keep = None
         if "obj" in kw and kw["obj"] is not None and not isinstance(kw["obj"], int):
-            p, mem, keep = _ptr(kw["obj"], np.float64)
+            p, mem, keep = _ptr(kw["obj"], np.float64, self.problem.device)
             cp.obj, cp.obj_mem = p, mem
         r, before, after = Result(), Stats(), Stats()
         _check(lib().cpd_corner_push(self.h, C.byref(cp), C.byref(r), C.byref(before), C.byref(after)))
@@ -358,12 +382,15 @@ class Solver:
 
     def get_iterate_device(self, x, y, z=None):
         """Copy into caller-owned torch CUDA tensors (device to device)."""
+        for a in (x, y, z):
+            if a is not None:
+                _ptr(a, np.float64, self.problem.device)   # dtype / contiguity / device checks
         _check(lib().cpd_get_iterate(self.h, x.data_ptr(), y.data_ptr(),
                                      z.data_ptr() if z is not None else None, DEVICE))
 
     def set_iterate(self, x=None, y=None):
-        px, mx, kx = _ptr(x, np.float64)
-        py, my, ky = _ptr(y, np.float64)
+        px, mx, kx = _ptr(x, np.float64, self.problem.device)
+        py, my, ky = _ptr(y, np.float64, self.problem.device)
         mem = mx if x is not None else my
         _check(lib().cpd_set_iterate(self.h, px, py, mem))
 

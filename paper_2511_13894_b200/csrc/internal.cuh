@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -124,6 +125,9 @@ struct cpd_problem {
     bool uniform_bounds = false;
     double l0 = 0.0, u0 = 0.0;
     int num_sms = 148;
+    // solvers created on this problem and not yet destroyed: their captured graphs
+    // hold device pointers of the problem, so scale / set_senses refuse while > 0
+    mutable std::atomic<int> live_solvers{0};
     // ---- distribution.  Side 0 = m-side (rows of A: y, b, Ax),
     // side 1 = n-side (rows of A^T: x, c, bounds).  The local matrices are this
     // rank's block: row-block (split = 1) keeps rows R_p of A, so A has m_p rows and

@@ -25,6 +25,16 @@ namespace cpd {
 #define CPD_SLAB_COLS (4 << 20)
 #endif
 constexpr int64_t SLAB_COLS = CPD_SLAB_COLS;
+// Runtime overrides of the plan thresholds (env CPD_SLAB_COLS, CPD_HEAVY_MIN), read at
+// plan build: the parity tests use them to route reduced LPs through the engine paths
+// that only the full-size configs reach by default (multi-slab long pieces, k_dense).
+static int64_t env_i64(const char* name, int64_t dflt)
+{
+    const char* e = getenv(name);
+    return (e && *e) ? std::max<int64_t>(1, atoll(e)) : dflt;
+}
+static int64_t slab_cols() { return env_i64("CPD_SLAB_COLS", SLAB_COLS); }
+static int64_t heavy_min() { return env_i64("CPD_HEAVY_MIN", HEAVY_MIN); }
 #ifndef CPD_SLAB_MIN
 #define CPD_SLAB_MIN 0   // long rows shorter than this are not cut at column-slab boundaries
 #endif
@@ -170,14 +180,16 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     flush(rows);
     // long rows: slab boundaries (device binary search), pieces
     const int32_t nl = (int32_t)lrows.size();
-    const int32_t nslab = (int32_t)std::max<int64_t>(1, ((int64_t)cols + SLAB_COLS - 1) / SLAB_COLS);
+    const int64_t SLABW = slab_cols();
+    const int32_t nslab = (int32_t)std::max<int64_t>(1, ((int64_t)cols + SLABW - 1) / SLABW);
     const int32_t nb = nslab - 1;
     std::vector<int32_t> pos((size_t)nl * std::max(nb, 0));
     if (nl > 0 && nb > 0) {
         DBuf<int32_t> dl(nl), dpos((size_t)nl * nb);
         CPD_CUDA(cudaMemcpy(dl.p, lrows.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice));
         const int64_t tot = (int64_t)nl * nb;
-        k_slab_pos<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256>>>(nl, nb, dl.p, d_p, d_col, dpos.p);
+        k_slab_pos<<<(int)std::min<int64_t>((tot + 255) / 256, 4096), 256>>>(nl, nb, dl.p, d_p, d_col, dpos.p,
+                                                                               SLABW);
         CPD_CUDA(cudaGetLastError());
         CPD_CUDA(cudaMemcpy(pos.data(), dpos.p, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost));
     }
@@ -188,7 +200,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     std::vector<char> is_heavy(nl, 0);
     if (warp && cols >= 2 * HB)
         for (int32_t l = 0; l < nl; ++l)
-            if ((int64_t)rp[lrows[l] + 1] - rp[lrows[l]] >= HEAVY_MIN) {
+            if ((int64_t)rp[lrows[l] + 1] - rp[lrows[l]] >= heavy_min()) {
                 heavy_l.push_back(l);
                 is_heavy[l] = 1;
             }
@@ -301,7 +313,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     const char* sse = getenv("CPD_SHORT_SLABS");
     const int64_t nreq = sse ? atoll(sse) : CPD_SHORT_SLABS;
     const int32_t nss = nreq <= 0 ? nslab : (int32_t)std::min<int64_t>(nreq, std::max<int64_t>(1, cols));
-    const int64_t sw = nreq <= 0 ? SLAB_COLS : ((int64_t)cols + nss - 1) / nss;
+    const int64_t sw = nreq <= 0 ? slab_cols() : ((int64_t)cols + nss - 1) / nss;
     plan.short_ilv = nreq <= 0 ? 1 : 0;
     plan.short_nslab = nss;
     plan.short_width = sw;

@@ -20,7 +20,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -130,6 +132,29 @@ void Ctx::set_i32(int32_t* f, int32_t v)
 void Ctx::sync() { CPD_CUDA(cudaStreamSynchronize(st)); }
 
 static std::mutex g_grid_mu;
+
+// Resident-CTA grid of `kernel` at (threads, dynamic smem) on the CURRENT device,
+// cached per (device, kernel, smem).  The max-dynamic-smem attribute is per device,
+// so it is set (once) on every device a kernel runs on.
+static int occ_grid(const void* kernel, int threads, size_t smem, int num_sms, int cap_per_sm = 0)
+{
+    int dev = 0;
+    CPD_CUDA(cudaGetDevice(&dev));
+    static std::map<std::tuple<int, const void*, size_t, int>, int> cache;
+    std::lock_guard<std::mutex> lk(g_grid_mu);
+    const auto key = std::make_tuple(dev, kernel, smem, threads);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (smem > 0)
+        CPD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int nb = 0;
+    CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem));
+    nb = std::max(1, nb);
+    if (cap_per_sm > 0) nb = std::min(nb, cap_per_sm);
+    const int g = nb * num_sms;
+    cache[key] = g;
+    return g;
+}
 #ifndef CPD_SLAB_MERGE
 #define CPD_SLAB_MERGE 1
 #endif
@@ -142,20 +167,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         // A^T gathers y: its hot prefix (hot-row renumbering) is staged in shared memory
         const int hot = (&M == &cx.P->AT) ? cx.P->hot : 0;
         const size_t hsm = (size_t)NV * hot * sizeof(double);
-        static int sgrid = 0, ssms = 0;
-        static size_t shsm = (size_t)-1;
-        {
-            std::lock_guard<std::mutex> lk(g_grid_mu);
-            if (!sgrid || ssms != cx.P->num_sms || shsm != hsm) {
-                CPD_CUDA(cudaFuncSetAttribute(k_sell<NV, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)hsm));
-                int nb = 0;
-                CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sell<NV, Epi>, TPB_SELL, hsm));
-                ssms = cx.P->num_sms;
-                shsm = hsm;
-                sgrid = std::max(1, nb) * ssms;
-            }
-        }
+        const int sgrid = occ_grid((const void*)k_sell<NV, Epi>, TPB_SELL, hsm, cx.P->num_sms);
         const int gr = std::max(1, std::min<int>(sgrid, (M.sell.nslice + 7) / 8));
         DevSell ds = M.dsell();
         ds.hot = hot;
@@ -166,16 +178,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         return;
     }
     if (dp.pslot == 1) {   // warp-item plan
-        static int wgrid = 0, wsms = 0;
-        {
-            std::lock_guard<std::mutex> lk(g_grid_mu);
-            if (!wgrid || wsms != cx.P->num_sms) {
-                int nb = 0;
-                CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_csrw<NV, Epi>, TPB_W, 0));
-                wsms = cx.P->num_sms;
-                wgrid = std::max(1, nb) * wsms;
-            }
-        }
+        const int wgrid = occ_grid((const void*)k_csrw<NV, Epi>, TPB_W, 0, cx.P->num_sms);
         Gate g0 = g;
         g0.active = nullptr;
         // one launch per item segment (rows items, then each column slab's pieces), so
@@ -187,20 +190,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         auto launch_dense = [&]() {
             if (dp.nheavy > 0) {   // heavy rows by dense column blocks (their slots, then k_finish)
                 const size_t DSM = (size_t)NV * HB * sizeof(double);
-                static int dgrid = 0, dsms = 0;
-                static size_t dsm_set = 0;
-                {
-                    std::lock_guard<std::mutex> lk(g_grid_mu);
-                    if (!dgrid || dsms != cx.P->num_sms || dsm_set != DSM) {
-                        CPD_CUDA(cudaFuncSetAttribute(k_dense<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                      (int)DSM));
-                        int nb = 0;
-                        CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dense<NV>, TPB_D, DSM));
-                        dsms = cx.P->num_sms;
-                        dsm_set = DSM;
-                        dgrid = std::max(1, nb) * dsms;
-                    }
-                }
+                const int dgrid = occ_grid((const void*)k_dense<NV>, TPB_D, DSM, cx.P->num_sms);
                 const int grd = std::max(1, dgrid);   // item-balanced: every CTA busy
                 k_dense<NV><<<grd, TPB_D, DSM, cx.st>>>(M.dev(), dp, M.cols, v0, v1, g0, cx.ctl);
                 CPD_CUDA(cudaGetLastError());
@@ -266,19 +256,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         return;
     }
     constexpr size_t SMEM = sizeof(SpmvSmem<NV, Epi::NVEC>);
-    static int grid = 0, sms = 0;
-    {
-        std::lock_guard<std::mutex> lk(g_grid_mu);
-        if (!grid || sms != cx.P->num_sms) {
-            CPD_CUDA(cudaFuncSetAttribute(k_spmv<NV, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)SMEM));
-            int nb = 0;
-            CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spmv<NV, Epi>, TPB_SP, SMEM));
-            nb = std::max(1, std::min(nb, 8));
-            sms = cx.P->num_sms;
-            grid = nb * sms;
-        }
-    }
+    const int grid = occ_grid((const void*)k_spmv<NV, Epi>, TPB_SP, SMEM, cx.P->num_sms, 8);
     const int gr = std::max(1, std::min(grid, dp.nent));
     k_spmv<NV, Epi><<<gr, TPB_SP, SMEM, cx.st>>>(M.dev(), dp, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p,
                                                  red);
@@ -1252,6 +1230,8 @@ int cpd_problem_set_senses(cpd_problem* p, const int8_t* sense, int32_t mem)
 {
     ABI_BEGIN
     if (!p || !sense) return fail(CPD_E_ARG, "NULL argument");
+    if (p->live_solvers.load() > 0)
+        return fail(CPD_E_STATE, "set_senses after a solver was created on this problem (destroy it first)");
     // this rank's local rows of A: all m (single GPU, col-block) or rows R_p (row-block)
     const int64_t off = p->split == 1 ? p->gofs[0] : 0;
     std::vector<int8_t> h((size_t)p->m);
@@ -1276,6 +1256,8 @@ int cpd_problem_scale(cpd_problem* p, int32_t ruiz_iters, int32_t pock_chambolle
     if (!p || ruiz_iters < 0 || ruiz_iters > 1000) return fail(CPD_E_ARG, "bad argument");
     if (p->split >= 0) return fail(CPD_E_ARG, "scaling of distributed problems is not supported");
     if (p->scaled) return fail(CPD_E_STATE, "problem is already scaled");
+    if (p->live_solvers.load() > 0)
+        return fail(CPD_E_STATE, "scale after a solver was created on this problem (destroy it first)");
     CPD_CUDA(cudaSetDevice(p->device));
     cpd::scale_problem(p, ruiz_iters, pock_chambolle ? 1 : 0);
     ABI_END
@@ -1353,6 +1335,26 @@ int cpd_problem_info(const cpd_problem* p, int64_t info[8])
     ABI_END
 }
 
+int cpd_problem_plan_info(const cpd_problem* p, int64_t out[12])
+{
+    ABI_BEGIN
+    if (!p || !out) return fail(CPD_E_ARG, "NULL argument");
+    const cpd::Plan& pl = p->A.plan;
+    out[0] = pl.warp;
+    out[1] = pl.nheavy;
+    out[2] = pl.nheavy > 0 ? pl.nhb : 0;
+    out[3] = pl.nslab;
+    out[4] = pl.short_on ? pl.short_nslab : 0;
+    out[5] = pl.nlong;
+    out[6] = pl.long_pieces;
+    out[7] = pl.rows_entries;
+    out[8] = p->AT.sell.on ? 1 : 0;
+    out[9] = p->hot;
+    out[10] = pl.warp ? 0 : pl.nent;
+    out[11] = 0;
+    ABI_END
+}
+
 void cpd_params_default(cpd_params* p)
 {
     if (!p) return;
@@ -1405,6 +1407,7 @@ int cpd_solver_create(const cpd_problem* p, const cpd_params* prm, cpd_solver** 
         return fail(CPD_E_ARG, "invalid parameter");
     CPD_CUDA(cudaSetDevice(p->device));
     *out = new cpd_solver(p, pr);
+    p->live_solvers.fetch_add(1);
     ABI_END
 }
 
@@ -1413,7 +1416,9 @@ int cpd_solver_destroy(cpd_solver* s)
     ABI_BEGIN
     if (s) {
         cudaSetDevice(s->P->device);
+        const cpd_problem* p = s->P;
         delete s;
+        p->live_solvers.fetch_sub(1);
     }
     ABI_END
 }

@@ -27,8 +27,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_2511_13894_b200 as cpd  # noqa: E402
 
 
-def close(a, b, rtol=1e-9):
-    return np.linalg.norm(a - b) <= rtol * np.linalg.norm(b) + 1e-14 * math.sqrt(b.size)
+from parity_util import close, worst  # noqa: E402  (norm AND entry-wise bound)
 
 
 @pytest.mark.parametrize("name,iters", [("c3", 6), ("c4", 6), ("c5", 4)])
@@ -57,3 +56,56 @@ def test_fullsize_lockstep(name, iters):
     for k in ("off_bound", "off_bound_strict", "zero_rc", "candidates", "est_primal_pushes",
               "est_dual_pushes", "is_candidate"):
         assert st[k] == ref[k], k
+
+
+def test_fullsize_c5_past_first_check():
+    """Full C5 in lockstep past the first default restart check (K = 64: 65 iterations,
+    the check's A / A^T passes, restart decision and omega update at k = 64)."""
+    lp = lpgen.config("c5")
+    olp = oracle.OracleLP(lp)
+    rng = np.random.default_rng(7)
+    x0 = np.minimum(np.maximum(rng.uniform(-1.0, 5.0, lp.n), lp.lb), lp.ub)
+    y0 = rng.standard_normal(lp.m)
+    eta = 0.9 / oracle.power_sigma(olp, 4, 7)
+    prm = dict(step_size=eta, restart=1)            # default K = 64
+    P = cpd.Problem.from_lp(lp)
+    S = cpd.Solver(P, **prm)
+    S.set_iterate(x0, y0)
+    R = oracle.Run(olp, oracle.default_params(**prm), x_init=x0, y_init=y0, mode=oracle.MODE_NONE)
+    for k in (64, 65):
+        S.step(k - R.k)
+        R.run(k - R.k)
+        xg, yg = S.get_iterate()
+        xo, yo = R.get()
+        assert close(xg, xo), (k, worst(xg, xo))
+        assert close(yg, yo), (k, worst(yg, yo))
+    assert R.restart_state()["restarts"] == 1   # the first check restarts (t = k)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_fullsize_termination(name):
+    """Phase 1 to eps_rel = 1e-4 at BASELINE size (SURVEY §8(c) parity item 2: C1 and C2
+    required, C3 when the oracle finishes in budget): status, iterations +-1%, pobj 1e-6."""
+    lp = lpgen.config(name)
+    olp = oracle.OracleLP(lp)
+    P = cpd.Problem.from_lp(lp)
+    S = cpd.Solver(P)
+    r = S.solve()
+    xo, yo, ro = oracle.solve(olp, oracle.default_params())
+    assert r["status"] == ro["status"] == 0, (r, ro)
+    assert abs(r["iterations"] - ro["iterations"]) <= max(1, 0.01 * ro["iterations"]), (r, ro)
+    assert r["pobj"] == pytest.approx(ro["pobj"], rel=1e-6)
+    assert r["returned_average"] == ro["returned_average"]
+    if name == "c2":
+        # Algorithm 1 + P:391-395 stop from the SAME phase-1 point at full C2 size
+        S.set_iterate(xo, yo)
+        rc, b, a = S.corner_push(seed=1001)
+        xh, _, z, rco, bo, ao, model = oracle.corner_push(olp, xo, yo, seed=1001)
+        assert rc["status"] == rco["status"] == 0
+        assert abs(rc["iterations"] - rco["iterations"]) <= max(1, 0.01 * rco["iterations"]), (rc, rco)
+        for k in ("fix_lb", "fix_ub", "off_bound", "zero_rc", "candidates", "is_candidate"):
+            assert b[k] == bo[k], k
+        xg, _, zg = S.get_iterate(z=True)
+        ref = oracle.stats(lp.m, xg, zg, lp.lb, lp.ub, model["lhat"], model["uhat"], 1e-6, 100_000)
+        for k in ("off_bound", "off_bound_strict", "off_bound_model", "zero_rc", "candidates"):
+            assert a[k] == ref[k], k

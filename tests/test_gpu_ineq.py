@@ -20,8 +20,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_2511_13894_b200 as cpd  # noqa: E402
 
 
-def close(a, b, rtol=1e-9):
-    return np.linalg.norm(a - b) <= rtol * np.linalg.norm(b) + 1e-14 * math.sqrt(b.size)
+from parity_util import close, worst  # noqa: E402  (norm AND entry-wise bound)
 
 
 @pytest.fixture(scope="module")

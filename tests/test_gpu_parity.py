@@ -28,8 +28,7 @@ ITER_RTOL = 1e-9
 CONFIGS = ["c1", "c2-s", "c3-s", "c4-s", "c5-s"]
 
 
-def close(a, b, rtol=ITER_RTOL):
-    return np.linalg.norm(a - b) <= rtol * np.linalg.norm(b) + 1e-14 * math.sqrt(b.size)
+from parity_util import close, worst  # noqa: E402  (norm AND entry-wise bound)
 
 
 @pytest.fixture(scope="module")

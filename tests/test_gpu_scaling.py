@@ -24,8 +24,7 @@ import paper_2511_13894_b200 as cpd  # noqa: E402
 NAMES = ["c1", "c2-s", "c4-s", "c5-s"]
 
 
-def close(a, b, rtol=1e-9):
-    return np.linalg.norm(a - b) <= rtol * np.linalg.norm(b) + 1e-14 * math.sqrt(b.size)
+from parity_util import close, worst  # noqa: E402  (norm AND entry-wise bound)
 
 
 @pytest.fixture(scope="module")
