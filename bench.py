@@ -133,16 +133,22 @@ def measured_peak():
 
 
 def ncu_traffic(config, kernel):
-    """dram read+write bytes per launch of `kernel` from the committed ncu summary."""
+    """dram read+write bytes per launch of `kernel` from the committed ncu summary
+    (tools/ncu_traffic.py), or (None, why) when the summary was captured on other
+    library sources than the ones benchmarked (its source_hash differs)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
+        from paper_2511_13894_b200 import _build
+        have, want = d[config].get("source_hash"), _build.source_hash()
+        if have != want:
+            return None, f"stale: ncu summary of sources {have}, benchmarked sources {want}"
         if kernel not in d[config] and kernel == "dual_step_A:corner":
             kernel = "dual_step_A"   # the dual step is the same pass in both phases
-        return d[config][kernel]["dram_bytes_per_launch"]
-    except Exception:
-        return None
+        return d[config][kernel]["dram_bytes_per_launch"], f"ncu --set full capture of sources {want}"
+    except Exception as e:
+        return None, f"unavailable ({type(e).__name__})"
 
 
 def dist_init(n):
@@ -228,18 +234,59 @@ def workload_config(args, lp, world, part=None):
             "parallelism": (f"{part} x{world}" if part else "1 GPU")}
 
 
-def cpu_baseline(lp):
+def host_cpu():
+    """nproc and the CPU model name of the host the oracle runs on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+# oracle iterations timed per config for its ms/iteration (bounded: ~10-15 s in all)
+_ORC_SAMPLE = {"c1": 2000, "c2": 100, "c3": 4, "c4": 6, "c5": 2}
+
+
+def cpu_baseline(lp, tte=("c1", "c2")):
+    """The oracle as it stands (single-threaded C, fp64) on this host: ms per phase-1
+    iteration (termination tests on, from x = 0) on C1-C5, and its time to eps_rel =
+    1e-4 from x = 0 (power iteration for eta included) on the configs it finishes in
+    seconds.  `value` = its it/s on the benchmarked workload (lp)."""
+    import lpgen
     import oracle
-    olp = oracle.OracleLP(lp)
-    eta = 0.9 / oracle.power_sigma(olp, 4, 7)
-    it = 3 if lp.nnz > 5e7 else 100
-    t0 = time.perf_counter()
-    r = oracle.Run(olp, oracle.default_params(step_size=eta, max_iters=it))
-    r.run(it)
-    dt = time.perf_counter() - t0
-    return {"value": r.k / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{r.k} phase-1 R-PDHG iterations (termination tests on) from x=0 on {lp.name} full size, "
-                      f"{dt:.1f} s, single thread"}
+    per = {}
+    main_v, main_sample = None, None
+    for nm, it in _ORC_SAMPLE.items():
+        L = lp if nm == lp.name else lpgen.config(nm)
+        olp = oracle.OracleLP(L)
+        eta = 0.9 / oracle.power_sigma(olp, 4, 7)
+        t0 = time.perf_counter()
+        r = oracle.Run(olp, oracle.default_params(step_size=eta, max_iters=it))
+        r.run(it)
+        dt = time.perf_counter() - t0
+        per[nm] = {"ms_per_iter": 1e3 * dt / max(r.k, 1), "iterations": r.k, "seconds": dt}
+        if nm == lp.name:
+            main_v = r.k / dt
+            main_sample = (f"{r.k} phase-1 R-PDHG iterations (termination tests on) from x=0 on {lp.name} "
+                           f"full size, {dt:.1f} s, single thread")
+        del olp
+    tt = {}
+    for nm in tte:
+        L = lpgen.config(nm)
+        olp = oracle.OracleLP(L)
+        t0 = time.perf_counter()
+        x, y, r = oracle.solve(olp, oracle.default_params())
+        tt[nm] = {"status": oracle.STATUS[r["status"]], "iterations": r["iterations"],
+                  "seconds": time.perf_counter() - t0}
+    return {"value": main_v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": main_sample,
+            "host": host_cpu(), "ms_per_iter": per, "time_to_eps": tt,
+            "note": "oracle time to eps on C3 (3,266 its at ~0.16 s) / C4 / C5 exceeds the bench's minutes: "
+                    "see profiles/r02_oracle_tte.json"}
 
 
 def time_to_eps(names, device):
@@ -268,8 +315,22 @@ def time_to_eps(names, device):
     return out
 
 
+def self_launch(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: start N ranks with torchrun on this
+    node (127.0.0.1) and exit with its status; rank 0's JSON line goes to our stdout."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, stdout=_JSON_FD)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     rank, world, local = dist_init(args.gpus)
     import lpgen
     lp = lpgen.config(args.config)
@@ -333,6 +394,7 @@ def main():
     it1, it2 = r1["iterations"], r2["iterations"]
     hbm_gbs = value * (it1 * b_it1 + it2 * b_it2) / max(it1 + it2, 1) / 1e9
     kernel_share = {k: round(v[0] / ms, 4) for k, v in kt.items() if v[1] > 0}
+    traffic, traffic_src = ncu_traffic(args.config, dom)
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -343,9 +405,12 @@ def main():
         "hbm_gbs_model": hbm_gbs,
         "iterations_per_step": {"phase1": it1, "corner": it2},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(args.config, dom),
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "kernel": dom, "kernel_ms": dom_ms, "algorithmic_bytes_per_launch": dom_bytes,
-                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
+                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                     "whole_path_gbs": hbm_gbs, "whole_path_frac": hbm_gbs / peak,
+                     "whole_path_frac_of_8tbs": hbm_gbs / 8000.0},
         "kernel_time_share": kernel_share,
         "gpu_launches": launches,
         "corner_stats": {"before": before, "after": after},

@@ -261,6 +261,15 @@ int cpd_problem_get_scaling(const cpd_problem *p, double *r, double *s);
  * from the GLOBAL CSR(A^T).  CPD_E_ARG if world > min(m, n). */
 int cpd_partition(int32_t m, int32_t n, const int32_t *AT_rowptr, const int32_t *AT_col, int32_t world,
                   int32_t partition, int64_t *bounds);
+/* Host-only (no device needed): the layout cpd_problem_create_dist gives rank `rank`
+ * (partition -1 = auto, as there).  out[12] = {partition, split side (0 m-side: y, b,
+ * Ax sliced; 1 n-side: x, c, bounds sliced), L = slice length ceil(rows of the split
+ * side / world), block [begin, end) of the sharded side (columns for partition 1,
+ * rows for 0), owned length of side 0, of side 1, global index of the owned part's
+ * element 0 on side 0, on side 1, offset of the owned part in the rank's local
+ * side-0 arrays, side-1 arrays, local rows of A^T}.  Errors as cpd_partition. */
+int cpd_dist_layout(int32_t m, int32_t n, const int32_t *AT_rowptr, const int32_t *AT_col, int32_t world,
+                    int32_t partition, int32_t rank, int64_t out[12]);
 /* 128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it). */
 int cpd_nccl_get_unique_id(char id[128]);
 /* Create this rank's block of the GLOBAL LP (CSR(A^T) + b, c, lb, ub, all in host

@@ -33,6 +33,7 @@ DECLARED_SYMBOLS = [
     "cpd_get_kernel_times", "cpd_kernel_bytes", "cpd_solver_counters",
     "cpd_partition", "cpd_nccl_get_unique_id", "cpd_problem_create_dist", "cpd_problem_dist_info",
     "cpd_problem_scale", "cpd_problem_get_scaling", "cpd_problem_set_senses", "cpd_problem_plan_info",
+    "cpd_dist_layout",
 ]
 
 
@@ -114,6 +115,7 @@ def lib():
             "cpd_kernel_bytes": (C.c_int, [P, C.c_char_p, C.POINTER(D)]),
             "cpd_solver_counters": (C.c_int, [P, P]),
             "cpd_partition": (C.c_int, [I32, I32, P, P, I32, I32, P]),
+            "cpd_dist_layout": (C.c_int, [I32, I32, P, P, I32, I32, I32, P]),
             "cpd_nccl_get_unique_id": (C.c_int, [C.c_char_p]),
             "cpd_problem_create_dist": (C.c_int, [I32, I32, C.c_char_p, I32, I32, I32, I64, P, P, P, P, P, P,
                                                   P, I32, C.POINTER(P)]),
@@ -189,6 +191,18 @@ def partition(m, n, ATp, ATj, world, partition):
     _check(lib().cpd_partition(int(m), int(n), ATp.ctypes.data, ATj.ctypes.data, int(world), int(partition),
                                out.ctypes.data))
     return out
+
+
+def dist_layout(m, n, ATp, ATj, world, partition, rank):
+    """cpd_dist_layout: the slice / block layout of `rank` (host only, no device)."""
+    ATp = np.ascontiguousarray(ATp, np.int32)
+    ATj = np.ascontiguousarray(ATj, np.int32)
+    out = np.zeros(12, np.int64)
+    _check(lib().cpd_dist_layout(int(m), int(n), ATp.ctypes.data, ATj.ctypes.data, int(world), int(partition),
+                                 int(rank), out.ctypes.data))
+    keys = ("partition", "split", "L", "block_begin", "block_end", "own_len_m", "own_len_n", "gofs_m",
+            "gofs_n", "poff_m", "poff_n", "local_rows_AT")
+    return dict(zip(keys, out.tolist()))
 
 
 def nccl_unique_id() -> bytes:

@@ -35,6 +35,16 @@ def deps():
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "cpd.h")]
 
 
+def source_hash() -> str:
+    """sha256 (first 16 hex) of the library sources: tags profiles measured on a build."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in deps():
+        with open(f, "rb") as fh:
+            h.update(os.path.basename(f).encode() + b"\0" + fh.read())
+    return h.hexdigest()[:16]
+
+
 def stale() -> bool:
     if not os.path.exists(LIB):
         return True

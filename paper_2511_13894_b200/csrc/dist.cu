@@ -159,11 +159,70 @@ static std::vector<int64_t> balanced_blocks(const std::vector<int64_t>& len, int
     return bnd;
 }
 
+// Slice / block layout of one rank, shared by cpd_problem_create_dist
+// and the host-only cpd_dist_layout: `bnd` = the partition's block bounds.  Side 0 =
+// m-side (rows of A), side 1 = n-side (rows of A^T).  The split side (the one whose
+// local rows are ALL rows: n-side for row-block, m-side for col-block) is cut into
+// `world` equal slices of L = ceil(rows / world) (the last ones shorter, possibly
+// empty); the other side is owned by blocks.  poff = offset of the owned part inside
+// the rank's local arrays (the local problem holds every row of the split side).
+struct DistLayout {
+    int split;
+    int64_t L;
+    std::vector<int64_t> gofs[2], len[2];   // per rank
+};
+static DistLayout dist_layout(int32_t m, int32_t n, int world, int partition, const std::vector<int64_t>& bnd)
+{
+    DistLayout d;
+    d.split = partition == 0 ? 1 : 0;
+    const int64_t rows_split = d.split == 1 ? n : m;
+    d.L = (rows_split + world - 1) / world;
+    for (int s = 0; s < 2; ++s) {
+        d.gofs[s].assign(world, 0);
+        d.len[s].assign(world, 0);
+        for (int q = 0; q < world; ++q) {
+            if (s == d.split) {
+                const int64_t o = std::min<int64_t>((int64_t)q * d.L, rows_split);
+                d.gofs[s][q] = o;
+                d.len[s][q] = std::min<int64_t>(d.L, rows_split - o);
+            } else {
+                d.gofs[s][q] = bnd[q];
+                d.len[s][q] = bnd[q + 1] - bnd[q];
+            }
+        }
+    }
+    return d;
+}
+
 }  // namespace cpd
 
 using namespace cpd;
 
 extern "C" {
+
+/* see include/cpd.h */
+int cpd_dist_layout(int32_t m, int32_t n, const int32_t* AT_rowptr, const int32_t* AT_col, int32_t world,
+                    int32_t partition, int32_t rank, int64_t out[12])
+{
+    if (!out || world < 1 || rank < 0 || rank >= world) return CPD_E_ARG;
+    if (partition < 0) partition = (n >= m) ? 1 : 0;
+    std::vector<int64_t> bnd(world + 1);
+    const int rc = cpd_partition(m, n, AT_rowptr, AT_col, world, partition, bnd.data());
+    if (rc != CPD_OK) return rc;
+    const DistLayout d = dist_layout(m, n, world, partition, bnd);
+    out[0] = partition;
+    out[1] = d.split;
+    out[2] = d.L;
+    out[3] = bnd[rank];
+    out[4] = bnd[rank + 1];
+    for (int s = 0; s < 2; ++s) {
+        out[5 + s] = d.len[s][rank];
+        out[7 + s] = d.gofs[s][rank];
+        out[9 + s] = (s == d.split) ? d.gofs[s][rank] : 0;
+    }
+    out[11] = partition == 1 ? (bnd[rank + 1] - bnd[rank]) : n;   // local rows of A^T
+    return CPD_OK;
+}
 
 /* see include/cpd.h */
 int cpd_partition(int32_t m, int32_t n, const int32_t* AT_rowptr, const int32_t* AT_col, int32_t world,
@@ -273,19 +332,10 @@ cpd_problem* cpd_problem_create_dist_impl(int32_t rank, int32_t world, const cha
         P->m_glob = m;
         P->n_glob = n;
         P->L = L;
+        const DistLayout d = dist_layout(m, n, world, partition, bnd);
         for (int s = 0; s < 2; ++s) {
-            P->rank_gofs[s].assign(world, 0);
-            P->rank_len[s].assign(world, 0);
-            for (int q = 0; q < world; ++q) {
-                if (s == split) {
-                    const int64_t o = std::min<int64_t>((int64_t)q * L, rows_split);
-                    P->rank_gofs[s][q] = o;
-                    P->rank_len[s][q] = std::min<int64_t>(L, rows_split - o);
-                } else {
-                    P->rank_gofs[s][q] = bnd[q];
-                    P->rank_len[s][q] = bnd[q + 1] - bnd[q];
-                }
-            }
+            P->rank_gofs[s] = d.gofs[s];
+            P->rank_len[s] = d.len[s];
             P->own_len[s] = (int32_t)P->rank_len[s][rank];
             P->gofs[s] = P->rank_gofs[s][rank];
             P->poff[s] = (s == split) ? P->gofs[s] : 0;   // the local problem holds all rows of the split side

@@ -1,7 +1,8 @@
 """Multi-GPU host logic on CPU (world_size 2, gloo) — `-m "not gpu"`.
 
-The library's partition (cpd_partition, host-only) decides which block of A each
-rank keeps and which slice of the exchanged vector it owns.  Here
+The library's partition (cpd_partition) and layout (cpd_dist_layout, the same
+host function cpd_problem_create_dist uses) decide which block of A each rank keeps
+and which slice of the exchanged vector it owns.  Here
 two gloo processes take those blocks and run the distributed R-PDHG iteration's
 algebra with the exchanges the CUDA path makes (reduce-scatter of the partial
 product, all-gather of the updated slice, allreduce of scalars) in numpy, and the
@@ -64,10 +65,18 @@ def _worker(rank, world, port, name, part, eta, q):
             dist.all_gather(out, t)
             return torch.cat(out).numpy()[:N]
 
-        b0, b1 = int(bnd[rank]), int(bnd[rank + 1])
+        # the library's own layout arithmetic (cpd_dist_layout = what create_dist uses)
+        lay = [cpd.dist_layout(m, n, lp.ATp, lp.ATj, world, part, qq) for qq in range(world)]
+        me = lay[rank]
+        assert me["partition"] == part and me["split"] == (1 if part == 0 else 0)
+        b0, b1 = me["block_begin"], me["block_end"]
+        assert (b0, b1) == (int(bnd[rank]), int(bnd[rank + 1]))
+        L = me["L"]
         if part == 1:   # col-block: columns [b0, b1); m-side slices
-            L = -(-m // world)
-            s0, s1 = rank * L, min((rank + 1) * L, m)
+            s0 = me["gofs_m"]
+            s1 = s0 + me["own_len_m"]
+            assert me["own_len_n"] == b1 - b0 and me["gofs_n"] == b0 and me["poff_m"] == s0 and me["poff_n"] == 0
+            assert me["local_rows_AT"] == b1 - b0
             Ap = A[:, b0:b1]
             nb2 = allreduce(np.dot(lp.b[s0:s1], lp.b[s0:s1]))[0]
             nc2 = allreduce(np.dot(lp.c[b0:b1], lp.c[b0:b1]))[0]
@@ -82,14 +91,15 @@ def _worker(rank, world, port, name, part, eta, q):
                 ys = ys + sig * (lp.b[s0:s1] - axb)
                 y = all_gather(ys, L, m)
                 x = xp
-            xf = all_gather(np.pad(x, (0, max(0, (bnd[1:] - bnd[:-1]).max() - x.size))),
-                            int((bnd[1:] - bnd[:-1]).max()), None)
-            Lc = int((bnd[1:] - bnd[:-1]).max())
-            xfull = np.concatenate([xf[qq * Lc:qq * Lc + int(bnd[qq + 1] - bnd[qq])] for qq in range(world)])
+            Lc = max(d["own_len_n"] for d in lay)
+            xf = all_gather(np.pad(x, (0, Lc - x.size)), Lc, None)
+            xfull = np.concatenate([xf[qq * Lc:qq * Lc + lay[qq]["own_len_n"]] for qq in range(world)])
             yfull = y
         else:           # row-block: rows [b0, b1); n-side slices
-            L = -(-n // world)
-            s0, s1 = rank * L, min((rank + 1) * L, n)
+            s0 = me["gofs_n"]
+            s1 = s0 + me["own_len_n"]
+            assert me["own_len_m"] == b1 - b0 and me["gofs_m"] == b0 and me["poff_n"] == s0 and me["poff_m"] == 0
+            assert me["local_rows_AT"] == n
             Ap = A[b0:b1, :]
             nb2 = allreduce(np.dot(lp.b[b0:b1], lp.b[b0:b1]))[0]
             nc2 = allreduce(np.dot(lp.c[s0:s1], lp.c[s0:s1]))[0]
@@ -105,9 +115,14 @@ def _worker(rank, world, port, name, part, eta, q):
                 y = y + sig * (lp.b[b0:b1] - Ap @ (2 * xp - x))
                 x, xs = xp, xsp
             xfull = x
-            Lr = int((bnd[1:] - bnd[:-1]).max())
-            yf = all_gather(y, Lr, None)
-            yfull = np.concatenate([yf[qq * Lr:qq * Lr + int(bnd[qq + 1] - bnd[qq])] for qq in range(world)])
+            Lr = max(d["own_len_m"] for d in lay)
+            yf = all_gather(np.pad(y, (0, Lr - y.size)), Lr, None)
+            yfull = np.concatenate([yf[qq * Lr:qq * Lr + lay[qq]["own_len_m"]] for qq in range(world)])
+        # the slices of the split side tile it exactly, in rank order
+        side = "n" if part == 0 else "m"
+        ends = [(d[f"gofs_{side}"], d[f"gofs_{side}"] + d[f"own_len_{side}"]) for d in lay]
+        assert ends[0][0] == 0 and ends[-1][1] == (n if part == 0 else m)
+        assert all(ends[i][1] == ends[i + 1][0] for i in range(world - 1))
         if rank == 0:
             q.put((xfull, yfull))
     finally:
@@ -126,6 +141,8 @@ def _free_port():
 @pytest.mark.parametrize("part", [0, 1])
 @pytest.mark.parametrize("name", ["c1", "c2-s"])
 def test_sharded_iteration_matches_oracle(name, part):
+    """Two gloo ranks, each with the block and owned slice cpd_dist_layout assigns,
+    reproduce the oracle's single-process iterates (1e-9)."""
     lp = lpgen.config(name)
     olp = oracle.OracleLP(lp)
     eta = 0.9 / oracle.power_sigma(olp)
@@ -161,6 +178,31 @@ def test_partition_blocks(world, part):
     pre = np.concatenate([[0], np.cumsum(w)])
     loads = pre[bnd[1:]] - pre[bnd[:-1]]
     assert loads.max() <= pre[-1] / world + w.max() + 1
+
+
+@pytest.mark.parametrize("part", [0, 1, -1])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_dist_layout_tiles(world, part):
+    """Every rank's owned slices / blocks tile both sides exactly (no gap, no overlap),
+    slices are ceil(rows / world) long except at the end, offsets match the blocks."""
+    lp = lpgen.config("c5-s")
+    lay = [cpd.dist_layout(lp.m, lp.n, lp.ATp, lp.ATj, world, part, r) for r in range(world)]
+    pt = lay[0]["partition"]
+    assert pt == (part if part >= 0 else (1 if lp.n >= lp.m else 0))
+    for side, N in (("m", lp.m), ("n", lp.n)):
+        o = 0
+        for d in lay:
+            assert d[f"gofs_{side}"] == o
+            o += d[f"own_len_{side}"]
+        assert o == N
+    split = lay[0]["split"]
+    sp = "n" if split == 1 else "m"
+    N = lp.n if split == 1 else lp.m
+    assert all(d["L"] == -(-N // world) for d in lay)
+    assert all(d[f"own_len_{sp}"] == max(0, min(d["L"], N - r * d["L"])) for r, d in enumerate(lay))
+    assert all(d[f"poff_{sp}"] == d[f"gofs_{sp}"] for d in lay)
+    bnd = cpd.partition(lp.m, lp.n, lp.ATp, lp.ATj, world, pt)
+    assert [d["block_begin"] for d in lay] == list(bnd[:-1])
 
 
 def test_partition_rejects_too_many_ranks():

@@ -115,21 +115,26 @@ def test_forced_corner_lockstep(forced):
 
 
 def test_forced_termination_zipf(forced):
-    """A Zipf(1.2) LP (C5's recipe, reduced) through the forced engine paths, to
-    eps_rel = 1e-4: same status, iterations within +-1%, objective to 1e-6, and the
-    steering phase from the same phase-1 point stops at the same iteration +-1%."""
+    """A Zipf(1.2) LP (C5's recipe, reduced to 2,000 x 10,000) through the forced engine
+    paths, to eps_rel = 1e-4.  Plain R-PDHG does not get there (oracle: score 0.07 after
+    60,000 iterations: the Zipf head makes ||A|| huge), so both sides run with the
+    diagonal preconditioning (R-3; oracle: 20,352 iterations): same status,
+    iterations within +-1%, objective to 1e-6; then the steering phase from the same
+    phase-1 point stops at the same iteration +-1%."""
     *_, lpz, olpz, Pz = forced
     pz = Pz.plan_info()
     assert pz["heavy_rows"] >= 1 and pz["slabs"] >= 2, pz
-    S = cpd.Solver(Pz)
+    Pz.scale(10, 1)
+    S = cpd.Solver(Pz, max_iters=100000)
     r = S.solve()
-    xo, yo, ro = oracle.solve(olpz, oracle.default_params())
+    xo, yo, ro, sl = oracle.solve_scaled(olpz, oracle.default_params(max_iters=100000))
     assert r["status"] == ro["status"] == 0, (r, ro)
-    assert abs(r["iterations"] - ro["iterations"]) <= max(1, 0.01 * ro["iterations"])
+    assert abs(r["iterations"] - ro["iterations"]) <= max(1, 0.01 * ro["iterations"]), (r, ro)
     assert r["pobj"] == pytest.approx(ro["pobj"], rel=1e-6)
+    S.close()
     S2 = cpd.Solver(Pz)
     S2.set_iterate(xo, yo)
     rc, _, _ = S2.corner_push(seed=1001, candidate_floor=100)
-    _, _, _, rco, _, _, _ = oracle.corner_push(olpz, xo, yo, seed=1001, floor=100)
+    _, _, _, rco, _, _, _ = oracle.corner_push_scaled(olpz, sl, xo, yo, seed=1001, floor=100)
     assert rc["status"] == rco["status"] == 0
-    assert abs(rc["iterations"] - rco["iterations"]) <= max(1, 0.01 * rco["iterations"])
+    assert abs(rc["iterations"] - rco["iterations"]) <= max(1, 0.01 * rco["iterations"]), (rc, rco)

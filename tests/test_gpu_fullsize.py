@@ -82,10 +82,13 @@ def test_fullsize_c5_past_first_check():
     assert R.restart_state()["restarts"] == 1   # the first check restarts (t = k)
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2"])
 def test_fullsize_termination(name):
     """Phase 1 to eps_rel = 1e-4 at BASELINE size (SURVEY §8(c) parity item 2: C1 and C2
-    required, C3 when the oracle finishes in budget): status, iterations +-1%, pobj 1e-6."""
+    required; C3 only "when the oracle finishes within budget": its 3,266 iterations
+    at ~164 ms each are ~9 min of oracle, over the ~5 min a test may take, so C3's
+    termination is checked on c3-s in test_gpu_parity.py): status, iterations +-1%,
+    pobj 1e-6, and Algorithm 1 from the same phase-1 point."""
     lp = lpgen.config(name)
     olp = oracle.OracleLP(lp)
     P = cpd.Problem.from_lp(lp)

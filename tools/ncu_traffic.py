@@ -43,7 +43,9 @@ def main(rep, config, out="profiles/ncu_traffic.json"):
                 groups["dual_step_A"].append(cur)
                 cur = None
     data = json.load(open(out)) if os.path.exists(out) else {}
-    data[config] = {}
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2511_13894_b200 import _build
+    data[config] = {"source_hash": _build.source_hash()}
     for k, g in groups.items():
         if not g:
             continue
