@@ -347,8 +347,14 @@ class Problem:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().cpd_problem_destroy(self.h)
-            self.h = None
+            # solvers first (the C ABI refuses to free a problem with live solvers; a
+            # garbage-collected cycle may finalise the problem before its solvers)
+            for s in list(getattr(self, "_solvers", ())):
+                s.close()
+            if lib().cpd_problem_destroy(self.h) == 0:
+                self.h = None
+            else:   # a solver still alive (GC cleared the weak set first): its close() retries
+                self._pending_close = True
 
     def __del__(self):
         try:
@@ -366,6 +372,10 @@ class Solver:
         h = C.c_void_p()
         _check(lib().cpd_solver_create(problem.h, C.byref(self.params), C.byref(h)))
         self.h = h
+        import weakref
+        if not hasattr(problem, "_solvers"):
+            problem._solvers = weakref.WeakSet()
+        problem._solvers.add(self)
 
     def solve(self):
         r = Result()
@@ -448,6 +458,10 @@ class Solver:
         if getattr(self, "h", None):
             lib().cpd_solver_destroy(self.h)
             self.h = None
+            P = getattr(self, "problem", None)
+            if P is not None and getattr(P, "_pending_close", False):
+                P._pending_close = False
+                P.close()
 
     def __del__(self):
         try:

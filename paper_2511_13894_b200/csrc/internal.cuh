@@ -99,6 +99,8 @@ struct Sell {
     DBuf<double> val;
     int32_t nslice = 0;
     int64_t padded = 0;
+    int32_t r0 = 0, rows = 0;   // the rows [r0, r0 + rows) of the layout it holds
+    int32_t c0 = 0, c1 = 0;     // c1 > c0: only their entries in columns [c0, c1)
     bool on = false;
 };
 
@@ -108,9 +110,29 @@ struct Matrix {
     int32_t rows = 0, cols = 0;
     Plan plan;
     Sell sell;
+    Sell sell_short;   // warp plan: SELL-32 of the short-row suffix (replaces the rows items)
+    Sell sell_half[2]; // or the same rows split by column half (two passes, running sums)
+    DBuf<double> short_part;   // running sums of the short rows between the half passes
     DevCsr dev() const { return DevCsr{p.p, j.p, x.p, rows}; }
     DevSell dsell() const { return DevSell{sell.sp.p, sell.col.p, sell.val.p, rows, sell.nslice}; }
+    DevSell dsell_short() const
+    {
+        DevSell d{sell_short.sp.p, sell_short.col.p, sell_short.val.p, sell_short.rows, sell_short.nslice};
+        d.r0 = sell_short.r0;
+        return d;
+    }
+    // half pass h: h = 0 stores its sums in short_part, h = 1 starts from them
+    DevSell dsell_half(int h) const
+    {
+        const Sell& S = sell_half[h];
+        DevSell d{S.sp.p, S.col.p, S.val.p, S.rows, S.nslice};
+        d.r0 = S.r0;
+        if (h == 0) d.part = short_part.p; else d.init = short_part.p;
+        return d;
+    }
 };
+// SELL-32 of the short-row suffix of a warp-plan layout (rows sorted by length).
+void build_short_sell(Matrix& M, const std::vector<int32_t>& rp);
 // Build M.sell when the padded size is at most `max_ratio` x nnz (else M.sell.on = false).
 void build_sell(Matrix& M, int64_t nnz, double max_ratio);
 

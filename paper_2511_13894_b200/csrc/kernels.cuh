@@ -257,6 +257,21 @@ __device__ __forceinline__ double ld_stream(const double* p)
 #endif
 }
 
+// Bulk L2 prefetch of a byte range (cp.async.bulk.prefetch.L2, sm_90+): one
+// instruction, no registers or shared memory held, fire and forget.  The streamed
+// matrix ranges of the work item CPD_PF items ahead are pulled into L2 so the
+// dependent index -> gather chain of the item pays L2 latency, not DRAM latency.
+#ifndef CPD_PF
+#define CPD_PF 0
+#endif
+__device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes)
+{
+    if (bytes <= 0) return;
+    const uint64_t a = (uint64_t)p & ~15ull;
+    const uint64_t e = ((uint64_t)p + (uint64_t)bytes + 15ull) & ~15ull;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
+
 // KKT score terms (S-3): o = {rp, rd, pobj, dobj, r_p, r_d, r_g, score}
 __device__ __forceinline__ void score8(double rp2, double rd2, double pobj, double dobj,
                                        double nb, double nc, double* o)
@@ -896,6 +911,11 @@ struct DevSell {
     int32_t rows, nslice;
     double* push = nullptr;   // acc (m) when this pass pushes its short-row products
     int32_t hot = 0;          // gathered entries [0, hot) staged in shared memory (hot-row renumbering)
+    int32_t r0 = 0;           // the slices hold rows [r0, r0 + rows) of the layout (short-row suffix of A)
+    // column-split passes (short-row SELL by column half): the first pass stores its row
+    // sums in part[v * rows + rl] and skips the epilogue; the second starts from init
+    double* part = nullptr;
+    const double* init = nullptr;
 };
 
 constexpr int TPB_SELL = 256;
@@ -913,7 +933,7 @@ constexpr int SELL_U = CPD_SELL_U;   // entries per lane in flight
 template <int NV, class Epi>
 __global__ void __launch_bounds__(TPB_SELL, CPD_SELL_MINB)
 k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr,
-       double* red)
+       double* red, int prev, int fin)
 {
     constexpr int NS = Epi::NS;
     constexpr int NVEC = Epi::NVEC;
@@ -950,16 +970,22 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
     for (int s = (blockIdx.x * TPB_SELL + threadIdx.x) >> 5; s < M.nslice; s += nw) {
         const int64_t b = M.sp[s];
         const int len = (int)((M.sp[s + 1] - b) >> 5);
-        const int r = s * 32 + lane;
+        if (CPD_PF > 0 && lane == 0 && s + CPD_PF * nw < M.nslice) {
+            const int64_t pb = M.sp[s + CPD_PF * nw], pe = M.sp[s + CPD_PF * nw + 1];
+            l2_prefetch(M.col + pb, (pe - pb) * 4);
+            l2_prefetch(M.val + pb, (pe - pb) * 8);
+        }
+        const int rl = s * 32 + lane;   // row of the slice layout; r = row of the matrix
+        const int r = M.r0 + rl;
         // the epilogue's per-row inputs do not depend on the sum: load them now
         // (streamed, evict-first) into this warp's stage
         double* stg = vst[threadIdx.x >> 5];
 #if CPD_PRE
         double pre[NVEC > 0 ? NVEC : 1];   // in registers until the sum is done (no wait here)
 #pragma unroll
-        for (int v = 0; v < NVEC; ++v) pre[v] = (r < M.rows && vin[v]) ? __ldcs(vin[v] + r) : 0.0;
+        for (int v = 0; v < NVEC; ++v) pre[v] = (rl < M.rows && vin[v]) ? __ldcs(vin[v] + r) : 0.0;
 #else
-        if (r < M.rows)
+        if (rl < M.rows && !M.part)
 #pragma unroll
             for (int v = 0; v < NVEC; ++v) stg[v * 32 + lane] = vin[v] ? __ldcs(vin[v] + r) : 0.0;
 #endif
@@ -967,7 +993,7 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
         const double* vp = M.val + b + lane;
         double sm[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) sm[v] = 0.0;
+        for (int v = 0; v < NV; ++v) sm[v] = (M.init && rl < M.rows) ? __ldcs(M.init + (int64_t)v * M.rows + rl) : 0.0;
         // two-stage software pipeline over rounds of SELL_U entries per lane
         auto ldround = [&](int (&cc)[SELL_U], double (&aa)[SELL_U], int k0) {
 #pragma unroll
@@ -1001,7 +1027,13 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
                 a[u] = an[u];
             }
         }
-        if (r < M.rows) {
+        if (M.part) {   // first column pass: running sums only
+            if (rl < M.rows)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) __stcs(M.part + (int64_t)v * M.rows + rl, sm[v]);
+            continue;
+        }
+        if (rl < M.rows) {
             const double* vs[NVEC > 0 ? NVEC : 1];
 #pragma unroll
             for (int v = 0; v < NVEC; ++v) {
@@ -1022,7 +1054,11 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
             }
         }
     }
-    grid_finalize<NS, TPB_SELL>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+    if (M.part) return;   // first column pass: no epilogue, no partials
+    if (fin)
+        grid_finalize<NS, TPB_SELL>(acc, bpart, ctr, 0, red, [e, ctl](double* tot) { e.finalize(tot, ctl); });
+    else
+        block_partial<NS, TPB_SELL>(acc, bpart, prev);   // k_finish combines (short-row SELL of A)
 }
 
 // ------------------------------------------------------------ warp-item CSR SpMV + epilogue
@@ -1083,6 +1119,12 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
     for (int it = (blockIdx.x * TPB_W + threadIdx.x) >> 5; it < P.nent; it += nw) {
         const PlanEntry E = P.ent[it];
         const bool sl_item = sl_mode && E.b >= 0;
+        if (CPD_PF > 0 && lane == 0 && it + CPD_PF * nw < P.nent) {
+            const PlanEntry F = P.ent[it + CPD_PF * nw];
+            const bool fs = sl_mode && F.b >= 0;
+            l2_prefetch((fs ? P.short_col : M.j) + F.p0, (int64_t)(F.p1 - F.p0) * 4);
+            l2_prefetch((fs ? P.short_val : M.x) + F.p0, (int64_t)(F.p1 - F.p0) * 8);
+        }
         const int32_t* __restrict__ mj = sl_item ? P.short_col : M.j;
         const double* __restrict__ mx = sl_item ? P.short_val : M.x;
         const int p0 = E.p0, T = E.p1 - E.p0;   // (slab mode: P.ent = the slab's own items)
@@ -1285,6 +1327,11 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
         __syncthreads();
         for (int i = i0 + w; i < i1; i += NWD) {
             const PlanEntry E = P.dense_ent[i];
+            if (CPD_PF > 0 && lane == 0 && i + CPD_PF * NWD < ib) {
+                const PlanEntry F = P.dense_ent[i + CPD_PF * NWD];
+                l2_prefetch(M.j + F.p0, (int64_t)(F.p1 - F.p0) * 4);
+                l2_prefetch(M.x + F.p0, (int64_t)(F.p1 - F.p0) * 8);
+            }
             double sm[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) sm[v] = 0.0;

@@ -198,7 +198,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     const int32_t nhb = (int32_t)(((int64_t)cols + HB - 1) / HB);
     std::vector<int32_t> heavy_l;
     std::vector<char> is_heavy(nl, 0);
-    if (warp && cols >= 2 * HB)
+    if (warp && (cols >= 2 * HB || getenv("CPD_HEAVY_MIN")))   // (env: tests force k_dense on small n)
         for (int32_t l = 0; l < nl; ++l)
             if ((int64_t)rp[lrows[l] + 1] - rp[lrows[l]] >= heavy_min()) {
                 heavy_l.push_back(l);
@@ -376,26 +376,52 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
 }
 
 // ------------------------------------------------------------ SELL-32
-__global__ void k_sell_len(int32_t rows, int32_t nslice, const int32_t* p, int64_t* len)
+// entries [a, b) of row r with columns in [c0, c1) (columns ascending): [lo, hi)
+__device__ __forceinline__ void col_range(const int32_t* j, int32_t a, int32_t b, int32_t c0, int32_t c1,
+                                          int32_t& lo, int32_t& hi)
+{
+    int32_t l = a, h = b;
+    while (l < h) {
+        const int32_t mid = l + (h - l) / 2;
+        if (j[mid] < c0) l = mid + 1; else h = mid;
+    }
+    lo = l;
+    h = b;
+    while (l < h) {
+        const int32_t mid = l + (h - l) / 2;
+        if (j[mid] < c1) l = mid + 1; else h = mid;
+    }
+    hi = l;
+}
+
+__global__ void k_sell_len(int32_t rows, int32_t nslice, const int32_t* p, int64_t* len, int32_t r0 = 0,
+                           const int32_t* j = nullptr, int32_t c0 = 0, int32_t c1 = 0)
 {
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslice;
          s += (int64_t)gridDim.x * blockDim.x) {
         int32_t mx = 0;
         const int64_t r1 = std::min<int64_t>((s + 1) * 32, rows);
-        for (int64_t r = s * 32; r < r1; ++r) mx = max(mx, p[r + 1] - p[r]);
+        for (int64_t r = s * 32; r < r1; ++r) {
+            int32_t lo = p[r0 + r], hi = p[r0 + r + 1];
+            if (j) col_range(j, lo, hi, c0, c1, lo, hi);
+            mx = max(mx, hi - lo);
+        }
         len[s] = (int64_t)mx * 32;
     }
 }
 
-// one thread per (slice, lane): row r's entries, then padding (-1, 0.0)
+// one thread per (slice, lane): row r0 + r's entries, then padding (-1, 0.0)
 __global__ void k_sell_fill(int32_t rows, int32_t nslice, const int32_t* p, const int32_t* j, const double* x,
-                            const int64_t* sp, int32_t* scol, double* sval)
+                            const int64_t* sp, int32_t* scol, double* sval, int32_t r0 = 0, int32_t c0 = 0,
+                            int32_t c1 = 0)
 {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)nslice * 32;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = t >> 5, lane = t & 31, r = t;
         const int64_t b = sp[s], len = (sp[s + 1] - b) >> 5;
-        const int64_t q0 = r < rows ? p[r] : 0, n = r < rows ? p[r + 1] - p[r] : 0;
+        int32_t lo = r < rows ? p[r0 + r] : 0, hi = r < rows ? p[r0 + r + 1] : 0;
+        if (c1 > c0 && r < rows) col_range(j, lo, hi, c0, c1, lo, hi);
+        const int64_t q0 = lo, n = hi - lo;
         for (int64_t k = 0; k < len; ++k) {
             const int64_t d = b + k * 32 + lane;
             scol[d] = k < n ? j[q0 + k] : -1;
@@ -437,17 +463,21 @@ void mark_push(cpd_problem* P)
     P->push_on = true;
 }
 
-void build_sell(Matrix& M, int64_t nnz, double max_ratio)
+// SELL-32 of rows [r0, r0 + rows) of M's CSR into S (S.on = false when padding > max_ratio).
+static void build_sell_rows(const Matrix& M, Sell& S, int32_t r0, int32_t rows, int64_t nnz, double max_ratio,
+                            int32_t c0 = 0, int32_t c1 = 0)
 {
-    Sell& S = M.sell;
+    S.c0 = c0;
+    S.c1 = c1;
     S.on = false;
-    const int32_t rows = M.rows;
+    S.r0 = r0;
+    S.rows = rows;
     const int32_t ns = (int32_t)(((int64_t)rows + 31) / 32);
     if (nnz == 0 || rows == 0) return;
     DBuf<int64_t> len((size_t)ns + 1);
     CPD_CUDA(cudaMemset(len.p, 0, sizeof(int64_t) * ((size_t)ns + 1)));
     const int g = (int)std::min<int64_t>(((int64_t)ns + 255) / 256, 4096);
-    k_sell_len<<<g, 256>>>(rows, ns, M.p.p, len.p);
+    k_sell_len<<<g, 256>>>(rows, ns, M.p.p, len.p, r0, c1 > c0 ? M.j.p : nullptr, c0, c1);
     CPD_CUDA(cudaGetLastError());
     S.sp.alloc((size_t)ns + 1);
     size_t tb = 0;
@@ -461,14 +491,52 @@ void build_sell(Matrix& M, int64_t nnz, double max_ratio)
         S.sp.free();
         return;
     }
-    S.col.alloc((size_t)padded);
-    S.val.alloc((size_t)padded);
+    S.col.alloc((size_t)std::max<int64_t>(padded, 1));
+    S.val.alloc((size_t)std::max<int64_t>(padded, 1));
     const int g2 = (int)std::min<int64_t>(((int64_t)ns * 32 + 255) / 256, 65536);
-    k_sell_fill<<<g2, 256>>>(rows, ns, M.p.p, M.j.p, M.x.p, S.sp.p, S.col.p, S.val.p);
+    k_sell_fill<<<g2, 256>>>(rows, ns, M.p.p, M.j.p, M.x.p, S.sp.p, S.col.p, S.val.p, r0, c0, c1);
     CPD_CUDA(cudaGetLastError());
     CPD_CUDA(cudaDeviceSynchronize());
     S.nslice = ns;
     S.on = true;
+}
+
+void build_sell(Matrix& M, int64_t nnz, double max_ratio)
+{
+    build_sell_rows(M, M.sell, 0, M.rows, nnz, max_ratio);
+}
+
+// Short rows of a warp-plan layout whose rows are ordered by decreasing length (hot-row
+// renumbering): rows [r_s, rows) with <= WLONG nonzeros form a suffix, and their dual
+// step runs as a SELL-32 pass (lane = row, no segmented scan, no row search) instead of
+// the warp plan's rows items.  CPD_SSELL=0 keeps the rows items.
+void build_short_sell(Matrix& M, const std::vector<int32_t>& rp)
+{
+    M.sell_short.on = false;
+    M.sell_half[0].on = M.sell_half[1].on = false;
+    const char* e = getenv("CPD_SSELL");
+    if ((e && e[0] == '0') || !M.plan.warp) return;
+    const int32_t rows = M.rows;
+    int32_t rs = rows;
+    while (rs > 0 && (int64_t)rp[rs] - rp[rs - 1] <= WLONG) --rs;
+    for (int32_t r = 0; r < rs; ++r)   // suffix property: every earlier row is long
+        if ((int64_t)rp[r + 1] - rp[r] <= WLONG) return;
+    if (rs >= rows) return;
+    const int64_t nz = (int64_t)rp[rows] - rp[rs];
+    // two column halves (each half of the gathered vector L2-resident) when the vector
+    // is larger than ~64 MB; CPD_SSELL=1 forces one pass, =2 two
+    const bool halves = (e && e[0] == '2') || (!(e && e[0] == '1') && (int64_t)M.cols * 8 > (64ll << 20));
+    if (halves) {
+        const int32_t h = (M.cols + 1) / 2;
+        build_sell_rows(M, M.sell_half[0], rs, rows - rs, nz, 2.0, 0, h);
+        build_sell_rows(M, M.sell_half[1], rs, rows - rs, nz, 2.0, h, M.cols);
+        if (M.sell_half[0].on && M.sell_half[1].on) {
+            M.short_part.alloc(2 * ((size_t)rows - rs));   // [NV <= 2][short rows]
+            return;
+        }
+        M.sell_half[0].on = M.sell_half[1].on = false;
+    }
+    build_sell_rows(M, M.sell_short, rs, rows - rs, nz, 1.25);
 }
 
 // ------------------------------------------------------------ hot-row renumbering
@@ -505,10 +573,24 @@ thread_local bool g_no_renumber = false;
 // hold >= 30% of the nonzeros (C5's Zipf rows): the most-gathered entries of y then
 // form a prefix that k_sell keeps in shared memory.  Every y-side
 // array is stored in this internal order; the ABI maps y / b / senses / r.
-__global__ void k_len_keys(int32_t rows, const int32_t* p, int32_t maxlen, int32_t* key, int32_t* val)
+// ascending key = descending length; ties among short rows (<= WLONG entries) broken by
+// decreasing count of entries in the first column half [0, half), so a SELL slice of
+// 32 consecutive short rows is also even in each half (short-row SELL passes, §6)
+__global__ void k_len_keys(int32_t rows, const int32_t* p, const int32_t* col, int32_t half, int32_t maxlen,
+                           uint64_t* key, int32_t* val)
 {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-        key[r] = maxlen - (p[r + 1] - p[r]);   // ascending key = descending length
+        const int32_t a = p[r], b = p[r + 1], len = b - a;
+        uint64_t sec = 0;
+        if (len <= WLONG) {
+            int32_t lo = a, hi = b;   // first entry with col >= half
+            while (lo < hi) {
+                const int32_t mid = lo + (hi - lo) / 2;
+                if (col[mid] < half) lo = mid + 1; else hi = mid;
+            }
+            sec = (uint64_t)(WLONG - (lo - a));
+        }
+        key[r] = ((uint64_t)(maxlen - len) << 8) | sec;
         val[r] = (int32_t)r;
     }
 }
@@ -540,10 +622,11 @@ static void renumber_rows(cpd_problem* P, std::vector<int32_t>& hp)
     const int sms = P->num_sms;
     auto grid = [&](int64_t N) { return (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, (int64_t)sms * 16)); };
     // stable device sort by decreasing length (radix sort is stable)
-    DBuf<int32_t> key(m), key2(m), val(m), dperm(m), dpinv(m), nlen((size_t)m + 1), dnp((size_t)m + 1);
-    k_len_keys<<<grid(m), 256>>>(m, P->A.p.p, maxlen, key.p, val.p);
-    int end_bit = 1;
-    while ((1LL << end_bit) <= (long long)maxlen) ++end_bit;
+    DBuf<uint64_t> key(m), key2(m);
+    DBuf<int32_t> val(m), dperm(m), dpinv(m), nlen((size_t)m + 1), dnp((size_t)m + 1);
+    k_len_keys<<<grid(m), 256>>>(m, P->A.p.p, P->A.j.p, (int32_t)((P->n + 1) / 2), maxlen, key.p, val.p);
+    int end_bit = 9;
+    while ((1LL << (end_bit - 8)) <= (long long)maxlen) ++end_bit;
     size_t tb = 0;
     CPD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, val.p, dperm.p, m, 0, end_bit));
     DBuf<unsigned char> tmp(tb);
@@ -860,6 +943,18 @@ void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc)
     // derived copies of the values
     if (P->AT.sell.on) build_sell(P->AT, P->nnz, 1.25);
     if (P->A.sell.on) build_sell(P->A, P->nnz, 1.25);
+    if (P->A.sell_short.on) {   // the scaled values of the short-row suffix
+        const int32_t r0 = P->A.sell_short.r0, nr = P->A.sell_short.rows;
+        int32_t q[2];
+        CPD_CUDA(cudaMemcpy(&q[0], P->A.p.p + r0, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        CPD_CUDA(cudaMemcpy(&q[1], P->A.p.p + r0 + nr, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        build_sell_rows(P->A, P->A.sell_short, r0, nr, (int64_t)q[1] - q[0], 1e30);
+    }
+    for (int hh = 0; hh < 2; ++hh)
+        if (P->A.sell_half[hh].on) {
+            Sell& S = P->A.sell_half[hh];
+            build_sell_rows(P->A, S, S.r0, S.rows, (int64_t)1 << 62, 1e30, S.c0, S.c1);
+        }
     if (P->push_on) mark_push(P);
     for (Matrix* M : {&P->A, &P->AT})
         if (M->plan.short_on) {
@@ -1011,6 +1106,7 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         bool warpA = 4 * long_nnz >= nnz && nnz > 0;
         if (we) warpA = we[0] != '0';
         build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.x.p, P->A.plan, warpA);
+        build_short_sell(P->A, hp);
         tm.mark("plan A");
         // SELL-32 where the rows are short and even (padding <= 25%); CPD_SELL=0 disables
         const char* se = getenv("CPD_SELL");

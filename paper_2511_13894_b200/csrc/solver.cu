@@ -172,7 +172,7 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         DevSell ds = M.dsell();
         ds.hot = hot;
         if (PushRole<Epi>::v == 1) ds.push = cx.push_acc;
-        k_sell<NV, Epi><<<gr, TPB_SELL, hsm, cx.st>>>(ds, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p, red);
+        k_sell<NV, Epi><<<gr, TPB_SELL, hsm, cx.st>>>(ds, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p, red, 0, 1);
         CPD_CUDA(cudaGetLastError());
         ++cx.launches;
         return;
@@ -211,7 +211,30 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
             if (slab < 0 || (spass & 2)) prev += gr;   // only the last slab pass leaves partials
         };
         // (the short-row push, when on, already summed the rows items' products in K1)
-        if (M.plan.short_on && !(PushRole<Epi>::v == 2 && cx.push_acc)) {
+        if ((M.sell_short.on || M.sell_half[0].on) && !(PushRole<Epi>::v == 2 && cx.push_acc)) {
+            // short-row suffix as SELL-32 passes (lane = row): one pass, or one per
+            // column half (running sums between them), then the heavy rows' dense blocks
+            // and every long piece; k_finish combines and finalizes
+            const int sgrid = occ_grid((const void*)k_sell<NV, Epi>, TPB_SELL, 0, cx.P->num_sms);
+            auto sell_pass = [&](const DevSell& ds, int nslice, int fin) {
+                const int gr = std::max(1, std::min<int>(sgrid, (nslice + 7) / 8));
+                k_sell<NV, Epi><<<gr, TPB_SELL, 0, cx.st>>>(ds, v0, v1, epi, gs, cx.ctl, cx.bpart.p, cx.ctr.p, red,
+                                                            prev, fin);
+                CPD_CUDA(cudaGetLastError());
+                ++cx.launches;
+                gs.active = nullptr;
+                return gr;
+            };
+            if (M.sell_half[0].on) {
+                static_assert(NV <= 2, "short_part holds two vectors");
+                sell_pass(M.dsell_half(0), M.sell_half[0].nslice, 0);   // no partials
+                prev += sell_pass(M.dsell_half(1), M.sell_half[1].nslice, single ? 1 : 0);
+            } else {
+                prev += sell_pass(M.dsell_short(), M.sell_short.nslice, single ? 1 : 0);
+            }
+            launch_dense();
+            if (!single && seg.back() > seg[1]) launch_items(seg[1], seg.back(), 0);
+        } else if (M.plan.short_on && !(PushRole<Epi>::v == 2 && cx.push_acc)) {
             launch_dense();
             // the short rows' items once per column slab (each pass gathers from one
             // L2-resident slab of the vector), then every long piece
@@ -1314,8 +1337,11 @@ int cpd_problem_destroy(cpd_problem* p)
 {
     ABI_BEGIN
     if (p) {
+        if (p->live_solvers.load() > 0)   // their graphs and buffers point into the problem
+            return fail(CPD_E_STATE, "problem still has live solvers (destroy them first)");
         cudaSetDevice(p->device);
         delete p;
+        (void)cudaGetLastError();   // an error of the teardown is not the next call's error
     }
     ABI_END
 }
@@ -1419,6 +1445,7 @@ int cpd_solver_destroy(cpd_solver* s)
         const cpd_problem* p = s->P;
         delete s;
         p->live_solvers.fetch_sub(1);
+        (void)cudaGetLastError();
     }
     ABI_END
 }

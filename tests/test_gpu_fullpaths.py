@@ -30,7 +30,7 @@ from parity_util import close, worst  # noqa: E402
 
 FORCE = {"CPD_HEAVY_MIN": "4096", "CPD_SLAB_COLS": "8192", "CPD_WARP": "1", "CPD_SHORT": "1"}
 # a Zipf(1.2) LP the oracle solves to eps_rel = 1e-4 in seconds (same recipe as C5)
-ZIPF_TERM = dict(m=2000, n=10000, per_col=12, seed=25, ub=100.0, zipf=1.2, name="c5-xs")
+ZIPF_TERM = dict(m=3000, n=18000, per_col=12, seed=26, ub=100.0, zipf=1.2, name="c5-xs")
 
 
 @pytest.fixture(scope="module")
@@ -115,10 +115,11 @@ def test_forced_corner_lockstep(forced):
 
 
 def test_forced_termination_zipf(forced):
-    """A Zipf(1.2) LP (C5's recipe, reduced to 2,000 x 10,000) through the forced engine
-    paths, to eps_rel = 1e-4.  Plain R-PDHG does not get there (oracle: score 0.07 after
-    60,000 iterations: the Zipf head makes ||A|| huge), so both sides run with the
-    diagonal preconditioning (R-3; oracle: 20,352 iterations): same status,
+    """A Zipf(1.2) LP (C5's recipe, reduced to 3,000 x 18,000) through the forced engine
+    paths, to eps_rel = 1e-4.  Plain R-PDHG does not get there on these LPs (oracle, a
+    2,000 x 10,000 one: score 0.07 after 60,000 iterations; the Zipf head makes ||A||
+    huge), so both sides run with the diagonal preconditioning (R-3; oracle:
+    5,809 iterations, 8 s): same status,
     iterations within +-1%, objective to 1e-6; then the steering phase from the same
     phase-1 point stops at the same iteration +-1%."""
     *_, lpz, olpz, Pz = forced
@@ -138,3 +139,31 @@ def test_forced_termination_zipf(forced):
     _, _, _, rco, _, _, _ = oracle.corner_push_scaled(olpz, sl, xo, yo, seed=1001, floor=100)
     assert rc["status"] == rco["status"] == 0
     assert abs(rc["iterations"] - rco["iterations"]) <= max(1, 0.01 * rco["iterations"]), (rc, rco)
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+def test_short_row_sell_modes(mode, monkeypatch):
+    """The short-row suffix of A's warp plan: rows items (0), one SELL-32 pass (1) or two
+    column-half SELL passes with running sums (2, C5's default): 1e-9 lockstep with
+    restarts, check passes and power iteration included."""
+    monkeypatch.setenv("CPD_SSELL", mode)
+    monkeypatch.setenv("CPD_WARP", "1")
+    lp = lpgen.config("c5-s")
+    olp = oracle.OracleLP(lp)
+    P = cpd.Problem.from_lp(lp)
+    assert P.plan_info()["warp"] == 1
+    eta = 0.9 / oracle.power_sigma(olp)
+    S = cpd.Solver(P, step_size=eta, restart=1)
+    R = oracle.Run(olp, oracle.default_params(step_size=eta, restart=1), mode=oracle.MODE_NONE)
+    for k in (1, 64, 65, 300):
+        S.step(k - R.k)
+        R.run(k - R.k)
+        xg, yg = S.get_iterate()
+        xo, yo = R.get()
+        assert close(xg, xo) and close(yg, yo), (mode, k, worst(xg, xo), worst(yg, yo))
+    assert P.power_sigma(128, 7) == pytest.approx(oracle.power_sigma(olp, 128, 7), rel=1e-12)
+    S2 = cpd.Solver(P, max_iters=2000)
+    r = S2.solve()
+    _, _, ro = oracle.solve(olp, oracle.default_params(max_iters=2000))
+    assert r["status"] == ro["status"] and r["iterations"] == ro["iterations"]
+    assert r["pobj"] == pytest.approx(ro["pobj"], rel=1e-6)
