@@ -111,8 +111,7 @@ struct Matrix {
     Plan plan;
     Sell sell;
     Sell sell_short;   // warp plan: SELL-32 of the short-row suffix (replaces the rows items)
-    Sell sell_half[2]; // or the same rows split by column half (two passes, running sums)
-    DBuf<double> short_part;   // running sums of the short rows between the half passes
+    Sell sell_half[2]; // or the same rows split by column half (two passes, running sums in the Ctx)
     DevCsr dev() const { return DevCsr{p.p, j.p, x.p, rows}; }
     DevSell dsell() const { return DevSell{sell.sp.p, sell.col.p, sell.val.p, rows, sell.nslice}; }
     DevSell dsell_short() const
@@ -121,13 +120,13 @@ struct Matrix {
         d.r0 = sell_short.r0;
         return d;
     }
-    // half pass h: h = 0 stores its sums in short_part, h = 1 starts from them
-    DevSell dsell_half(int h) const
+    // half pass h: h = 0 stores its sums in buf, h = 1 starts from them
+    DevSell dsell_half(int h, double* buf) const
     {
         const Sell& S = sell_half[h];
         DevSell d{S.sp.p, S.col.p, S.val.p, S.rows, S.nslice};
         d.r0 = S.r0;
-        if (h == 0) d.part = short_part.p; else d.init = short_part.p;
+        if (h == 0) d.part = buf; else d.init = buf;
         return d;
     }
 };
@@ -226,6 +225,7 @@ struct Ctx {
     DBuf<unsigned> ctr;
     DBuf<double> lpartA, lpartAT;     // long-row piece partials of each layout
     DBuf<double> shortA, shortAT;     // running row sums of the short-row slab passes
+    DBuf<double> sshortA;             // running row sums of the short-row SELL half passes
     double* push_acc = nullptr;       // set around the primal/dual pair of a batch (short-row push)
     DBuf<double> red;                 // this rank's totals of the last reduction (distributed)
     DBuf<double> part, recv;          // reduce-scatter send [world][2][L] / receive [2][L] buffers

@@ -530,10 +530,7 @@ void build_short_sell(Matrix& M, const std::vector<int32_t>& rp)
         const int32_t h = (M.cols + 1) / 2;
         build_sell_rows(M, M.sell_half[0], rs, rows - rs, nz, 2.0, 0, h);
         build_sell_rows(M, M.sell_half[1], rs, rows - rs, nz, 2.0, h, M.cols);
-        if (M.sell_half[0].on && M.sell_half[1].on) {
-            M.short_part.alloc(2 * ((size_t)rows - rs));   // [NV <= 2][short rows]
-            return;
-        }
+        if (M.sell_half[0].on && M.sell_half[1].on) return;   // running sums: Ctx::sshortA
         M.sell_half[0].on = M.sell_half[1].on = false;
     }
     build_sell_rows(M, M.sell_short, rs, rows - rs, nz, 1.25);

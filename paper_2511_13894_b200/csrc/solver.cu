@@ -60,6 +60,7 @@ Ctx::Ctx(const cpd_problem* p) : P(p)
     lpartA.alloc((size_t)std::max<int64_t>(1, pa.long_pieces) * GW * 2);
     lpartAT.alloc((size_t)std::max<int64_t>(1, pt.long_pieces) * GW * 2);
     if (pa.short_on) shortA.alloc((size_t)2 * p->A.rows);
+    if (p->A.sell_half[0].on) sshortA.alloc((size_t)2 * p->A.sell_half[0].rows);
     if (pt.short_on) shortAT.alloc((size_t)2 * p->AT.rows);
     red.alloc(NSMAX);
     CPD_CUDA(cudaMemset(red.p, 0, sizeof(double) * NSMAX));
@@ -227,8 +228,8 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
             };
             if (M.sell_half[0].on) {
                 static_assert(NV <= 2, "short_part holds two vectors");
-                sell_pass(M.dsell_half(0), M.sell_half[0].nslice, 0);   // no partials
-                prev += sell_pass(M.dsell_half(1), M.sell_half[1].nslice, single ? 1 : 0);
+                sell_pass(M.dsell_half(0, cx.sshortA.p), M.sell_half[0].nslice, 0);   // no partials
+                prev += sell_pass(M.dsell_half(1, cx.sshortA.p), M.sell_half[1].nslice, single ? 1 : 0);
             } else {
                 prev += sell_pass(M.dsell_short(), M.sell_short.nslice, single ? 1 : 0);
             }
