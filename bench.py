@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--tte", default="c2,c3,c4", help="configs for the time-to-eps side measurement ('' = off)")
+    ap.add_argument("--tte", default="c2,c3,c4,c5", help="configs for the time-to-eps side measurement ('' = off)")
     ap.add_argument("--ref-iters", type=int, default=0, help="oracle iterations per reference step (0: auto)")
     ap.add_argument("--partition", type=int, default=-1,
                     help="multi-GPU partition: 0 row-block, 1 col-block, -1 auto (shard the long side)")
@@ -289,27 +289,49 @@ def cpu_baseline(lp, tte=("c1", "c2")):
                     "see profiles/r02_oracle_tte.json"}
 
 
-def time_to_eps(names, device):
+# phase-1 iteration cap of the time-to-eps runs (C5 does not reach eps in minutes:
+# it is reported as "not reached after N iterations" with its score)
+_TTE_CAP = {"c5": 4096}
+
+
+def time_to_eps(names, device, lp_cache=None):
     """Wall time from cpd_solve entry to return at eps_rel = 1e-4 (problem resident),
-    plain R-PDHG and with the diagonal preconditioning (cpd_problem_scale, NEXT-1)."""
+    plain R-PDHG and with the diagonal preconditioning (cpd_problem_scale, NEXT-1),
+    then Algorithm 1 from the phase-1 point with the P:391-395 stop: the Fig. 4 analogue
+    (steering / phase-1 iteration ratio) and the Fig. 1 analogue (off-bound
+    count before / after and its trajectory every 64 iterations)."""
     import lpgen
     import paper_2511_13894_b200 as cpd
     out = {}
     for nm in names:
-        lp = lpgen.config(nm)
+        lp = (lp_cache or {}).get(nm) or lpgen.config(nm)
+        cap = _TTE_CAP.get(nm, 200000)
         for tag, scale in (("", False), (":scaled", True)):
             P = cpd.Problem.from_lp(lp, device=device)
             if scale:
                 P.scale(10, 1)
-            S = cpd.Solver(P, max_iters=200000)
-            S.solve()   # warm-up (graph capture)
-            S.set_iterate(None, None)
+            S = cpd.Solver(P, max_iters=cap)
+            if nm not in _TTE_CAP:
+                S.solve()   # warm-up (graph capture)
+                S.set_iterate(None, None)
             r = S.solve()
-            rc, _, _ = S.corner_push(max_iters=200000)   # Algorithm 1 from the phase-1 point
-            out[nm + tag] = {"status": cpd.STATUS[r["status"]], "iterations": r["iterations"],
-                             "seconds": r["wall_s"], "it_per_s": r["iterations"] / r["wall_s"],
-                             "pobj": r["pobj"], "corner_status": cpd.STATUS[rc["status"]],
-                             "corner_iterations": rc["iterations"], "corner_seconds": rc["wall_s"]}
+            e = {"status": cpd.STATUS[r["status"]], "iterations": r["iterations"],
+                 "seconds": r["wall_s"], "it_per_s": r["iterations"] / r["wall_s"],
+                 "pobj": r["pobj"], "score": r["score"]}
+            if r["status"] != 0:
+                e["note"] = f"eps_rel=1e-4 not reached after {r['iterations']} iterations (score {r['score']:.3g})"
+            else:
+                rc, before, after = S.corner_push(max_iters=200000)   # Algorithm 1 from the phase-1 point
+                k, off, _ = S.trajectory()
+                e.update({"corner_status": cpd.STATUS[rc["status"]], "corner_iterations": rc["iterations"],
+                          "corner_seconds": rc["wall_s"],
+                          "corner_over_phase1": rc["iterations"] / max(r["iterations"], 1),
+                          "off_bound_before": before["off_bound"], "off_bound_after": after["off_bound"],
+                          "off_bound_model_after": after["off_bound_model"], "m": lp.m,
+                          "fix_lb": before["fix_lb"], "fix_ub": before["fix_ub"],
+                          "candidates": before["candidates"], "is_candidate": before["is_candidate"],
+                          "trajectory_off_bound": [int(v) for v in off[:: max(1, len(off) // 16)]]})
+            out[nm + tag] = e
             S.close()
             P.close()
     return out
@@ -426,7 +448,7 @@ def main():
         res["partition"] = {0: "row-block", 1: "col-block"}[P_info["partition"]]
     if args.tte and world == 1:
         try:
-            res["time_to_eps"] = time_to_eps([x for x in args.tte.split(",") if x], dev)
+            res["time_to_eps"] = time_to_eps([x for x in args.tte.split(",") if x], dev, {lp.name: lp})
         except Exception as e:  # pragma: no cover
             res["time_to_eps"] = {"error": str(e)}
     if not args.no_cpu_baseline and rank == 0 and world == 1:

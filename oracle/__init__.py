@@ -51,7 +51,9 @@ class Params(C.Structure):
                 ("power_iters", C.c_int32), ("seed", C.c_uint64),
                 ("primal_weight", C.c_double), ("restart", C.c_int32),
                 ("beta_suff", C.c_double), ("beta_nec", C.c_double),
-                ("beta_art", C.c_double), ("theta", C.c_double)]
+                ("beta_art", C.c_double), ("theta", C.c_double),
+                ("method", C.c_int32), ("reflection", C.c_double), ("pid", C.c_int32),
+                ("kp", C.c_double), ("ki", C.c_double), ("kd", C.c_double)]
 
 
 class Result(C.Structure):
@@ -101,6 +103,7 @@ def lib():
             L.orc_run.restype = C.c_int
             L.orc_run.argtypes = [P, C.c_int64]
             L.orc_get.argtypes = [P, P, P]
+            L.orc_get_z.argtypes = [P, P, P]
             L.orc_result_of.argtypes = [P, C.POINTER(Result)]
             L.orc_destroy.argtypes = [P]
             L.orc_get_eta.restype = C.c_double
@@ -137,7 +140,8 @@ def default_params(**kw) -> Params:
     """Defaults of SURVEY §8(b) cpd_params (same meaning as the CUDA side's)."""
     p = Params(eps_rel=1e-4, eps_abs=1e-6, max_iters=100000, time_limit_s=0.0, check_every=64,
                step_scale=0.9, step_size=0.0, power_iters=128, seed=7, primal_weight=0.0,
-               restart=1, beta_suff=0.2, beta_nec=0.8, beta_art=0.36, theta=0.5)
+               restart=1, beta_suff=0.2, beta_nec=0.8, beta_art=0.36, theta=0.5,
+               method=0, reflection=1.0, pid=0, kp=0.99, ki=0.01, kd=0.0)
     for k, v in kw.items():
         setattr(p, k, v)
     return p
@@ -260,6 +264,13 @@ class Run:
         x = np.zeros(self.olp.n)
         y = np.zeros(self.olp.m)
         lib().orc_get(self.h, _p(x), _p(y))
+        return x, y
+
+    def get_z(self):
+        """The internal iterate (Halpern: the Halpern sequence z, not T(z))."""
+        x = np.zeros(self.olp.n)
+        y = np.zeros(self.olp.m)
+        lib().orc_get_z(self.h, _p(x), _p(y))
         return x, y
 
     def result(self) -> dict:

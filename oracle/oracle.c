@@ -55,6 +55,11 @@ typedef struct {
     double primal_weight;    /* > 0: omega0 given explicitly */
     int32_t restart;         /* 0 none, 1 adaptive restart to average/current */
     double beta_suff, beta_nec, beta_art, theta;
+    /* NEXT-1 (cuPDLP+ lineage; reading H-1..H-4) */
+    int32_t method;          /* 0 R-PDHG (averages), 1 reflected restarted Halpern PDHG */
+    double reflection;       /* rho of z+ = lambda((1+rho) T(z) - rho z) + (1-lambda) z_anchor */
+    int32_t pid;             /* 1: PID primal weight at restarts (else theta smoothing) */
+    double kp, ki, kd;       /* PID gains on e = log(dy/dx) - log omega */
 } orc_params;
 
 typedef struct {
@@ -289,6 +294,10 @@ typedef struct {
     double *x, *y, *xavg, *yavg, *xr, *yr, *xn, *yn, *aty, *xbar, *axbar;
     int64_t k, t, restarts;
     double S_r, S_prev;
+    /* Halpern (method 1): anchor, last PDHG output T(z) = (xh, yh), fixed-point
+     * residuals r0 (at the anchor) / r_prev (last check), PID state */
+    double *xa, *ya, *xh, *yh, *dxv;
+    double r0, r_prev, r_last, pid_int, pid_eprev;
     int status, returned_average;
     double t0;
     /* scaled run (orc_set_original): score and primal residual on the ORIGINAL LP at
@@ -305,6 +314,7 @@ void orc_destroy(orc_state *s)
     free(s->x); free(s->y); free(s->xavg); free(s->yavg); free(s->xr); free(s->yr);
     free(s->xn); free(s->yn); free(s->aty); free(s->xbar); free(s->axbar);
     free(s->ux); free(s->uy);
+    free(s->xa); free(s->ya); free(s->xh); free(s->yh); free(s->dxv);
     free(s);
 }
 
@@ -345,6 +355,8 @@ orc_state *orc_create(const orc_lp *lp, const orc_params *prm, const double *c,
     s->y = (double *)calloc(M, 8); s->yavg = (double *)calloc(M, 8);
     s->yr = (double *)calloc(M, 8); s->yn = (double *)calloc(M, 8);
     s->axbar = (double *)calloc(M, 8);
+    s->xa = (double *)calloc(N, 8); s->xh = (double *)calloc(N, 8); s->dxv = (double *)calloc(N, 8);
+    s->ya = (double *)calloc(M, 8); s->yh = (double *)calloc(M, 8);
     s->t0 = now_s();
     s->nb = orc_norm2(m, lp->b);
     s->nc = orc_norm2(n, c);
@@ -357,6 +369,12 @@ orc_state *orc_create(const orc_lp *lp, const orc_params *prm, const double *c,
     for (int32_t i = 0; i < m; ++i) s->y[i] = y_init ? y_init[i] : 0.0;
     memcpy(s->xr, s->x, N * 8);
     memcpy(s->yr, s->y, M * 8);
+    memcpy(s->xa, s->x, N * 8);   /* Halpern anchor z^0 = starting point */
+    memcpy(s->ya, s->y, M * 8);
+    memcpy(s->xh, s->x, N * 8);
+    memcpy(s->yh, s->y, M * 8);
+    s->r0 = INFINITY; s->r_prev = INFINITY; s->r_last = INFINITY;
+    s->pid_int = 0.0; s->pid_eprev = 0.0;
     orc_score_t o;
     s->S_r = score_of(s, s->x, s->y, &o);
     s->S_prev = INFINITY;
@@ -372,12 +390,13 @@ int64_t orc_get_k(const orc_state *s) { return s->k; }
 
 /* Restart bookkeeping of a run (read-only test access for the restart pins,
  * tests/golden/restart_2x2.json): reference score S_r, previous candidate score
- * S_prev, iterations since the last restart t, and the restart count. */
+ * S_prev, iterations since the last restart t, and the restart count (Halpern: the
+ * fixed-point residuals r0 at the anchor and r_prev at the last check in S_r / S_prev). */
 void orc_get_restart_state(const orc_state *s, double *S_r, double *S_prev, int64_t *t,
                            int64_t *restarts)
 {
-    *S_r = s->S_r;
-    *S_prev = s->S_prev;
+    *S_r = s->prm.method == 1 ? s->r0 : s->S_r;
+    *S_prev = s->prm.method == 1 ? s->r_prev : s->S_prev;
     *t = s->t;
     *restarts = s->restarts;
 }
@@ -417,6 +436,111 @@ static double primal_res(orc_state *s, const double *x)
     return sqrt(r2);
 }
 
+/* Primal-weight update at a restart from the anchor movement (dx, dy): theta
+ * smoothing (S-1, PDLP lineage) or, with pid, a PID controller on the log-ratio error
+ * e = log(dy/dx) - log omega (reading H-3):
+ *   log omega <- log omega + kp e + ki sum(e) + kd (e - e_prev). */
+static void weight_update(orc_state *s, double dx, double dy)
+{
+    const orc_params *P = &s->prm;
+    if (!(dx > 1e-10 && dy > 1e-10)) return;
+    if (P->pid) {
+        double e = log(dy / dx) - log(s->omega);
+        s->pid_int += e;
+        double lw = log(s->omega) + P->kp * e + P->ki * s->pid_int + P->kd * (e - s->pid_eprev);
+        s->pid_eprev = e;
+        s->omega = exp(lw);
+    } else {
+        s->omega = exp(P->theta * log(dy / dx) + (1.0 - P->theta) * log(s->omega));
+    }
+}
+
+/* Reflected restarted Halpern PDHG (NEXT-1; readings H-1..H-4), step by step:
+ *   (xh, yh) = T(x, y)   (the PDHG map of R-PDHG: projected primal step, extrapolated dual step)
+ *   r^2 = ||xh-x||^2/tau + ||yh-y||^2/sigma + 2 <yh-y, A(xh-x)>   (fixed-point residual, M-norm)
+ *   lambda = (t+1)/(t+2);  z <- lambda((1+rho) zh - rho z) + (1-lambda) z_anchor;  t++, k++
+ *   r0 <- r when t was 0 (the residual at the anchor)
+ *   primal-only: stop at k >= min_iters with ||b - A xh|| <= target, returning zh
+ *   every K (t mod K = 0): score(zh) <= eps (mode full) -> return zh; restart test on r:
+ *     r <= b_suff r0, or (r <= b_nec r0 and r > r_prev), or t >= b_art k  ->
+ *     weight update from the anchor movement, z = z_anchor = zh, t = 0
+ *   k = max_iters -> return zh (ITER_LIMIT).  The returned point is always zh (in the box). */
+static int orc_run_halpern(orc_state *s, int64_t steps)
+{
+    const orc_lp *lp = s->lp;
+    int32_t m = lp->m, n = lp->n;
+    const orc_params *P = &s->prm;
+    const double rho = P->reflection;
+    for (int64_t it = 0; it < steps && s->status < 0; ++it) {
+        double tau = s->eta / s->omega;
+        double sigma = s->eta * s->omega;
+        /* (xh, yh) = T(z) */
+        orc_spmv(n, lp->ATp, lp->ATj, lp->ATx, s->y, s->aty);
+        for (int32_t j = 0; j < n; ++j)
+            s->xh[j] = proj(s->x[j] - tau * (s->c[j] - s->aty[j]), s->l[j], s->u[j]);
+        for (int32_t j = 0; j < n; ++j) s->xbar[j] = 2.0 * s->xh[j] - s->x[j];
+        orc_spmv(m, lp->Ap, lp->Aj, lp->Ax, s->xbar, s->axbar);
+        for (int32_t i = 0; i < m; ++i)
+            s->yh[i] = dual_proj(lp, i, s->y[i] + sigma * (lp->b[i] - s->axbar[i]));
+        int bad = 0;
+        for (int32_t j = 0; j < n; ++j) bad |= !isfinite(s->xh[j]);
+        for (int32_t i = 0; i < m; ++i) bad |= !isfinite(s->yh[i]);
+        if (bad) { s->status = 3; s->k += 1; break; }
+        /* fixed-point residual of z in the M-norm */
+        double dx2 = 0.0, dy2 = 0.0, cross = 0.0;
+        for (int32_t j = 0; j < n; ++j) { s->dxv[j] = s->xh[j] - s->x[j]; dx2 += s->dxv[j] * s->dxv[j]; }
+        orc_spmv(m, lp->Ap, lp->Aj, lp->Ax, s->dxv, s->axbar);   /* A (xh - x) */
+        for (int32_t i = 0; i < m; ++i) {
+            double d = s->yh[i] - s->y[i];
+            dy2 += d * d;
+            cross += d * s->axbar[i];
+        }
+        double r2 = dx2 / tau + dy2 / sigma + 2.0 * cross;
+        double r = sqrt(r2 > 0.0 ? r2 : 0.0);
+        if (s->t == 0) s->r0 = r;
+        s->r_last = r;
+        /* Halpern step with reflection */
+        double lam = (double)(s->t + 1) / (double)(s->t + 2);
+        for (int32_t j = 0; j < n; ++j)
+            s->x[j] = lam * ((1.0 + rho) * s->xh[j] - rho * s->x[j]) + (1.0 - lam) * s->xa[j];
+        for (int32_t i = 0; i < m; ++i)
+            s->y[i] = lam * ((1.0 + rho) * s->yh[i] - rho * s->y[i]) + (1.0 - lam) * s->ya[i];
+        s->t += 1;
+        s->k += 1;
+        orc_score_t o;
+        if (s->mode == MODE_PRIMAL_ONLY) {
+            if (s->k >= s->min_iters && primal_res(s, s->xh) <= s->target) { s->status = 0; break; }
+        }
+        if (s->t % P->check_every == 0) {
+            double S = score_of(s, s->xh, s->yh, &o);
+            if (s->mode == MODE_FULL && S <= P->eps_rel) { s->status = 0; break; }
+            if (P->restart) {
+                if (r <= P->beta_suff * s->r0 || (r <= P->beta_nec * s->r0 && r > s->r_prev) ||
+                    (double)s->t >= P->beta_art * (double)s->k) {
+                    double ddx = 0.0, ddy = 0.0;
+                    for (int32_t j = 0; j < n; ++j) { double d = s->xh[j] - s->xa[j]; ddx += d * d; }
+                    for (int32_t i = 0; i < m; ++i) { double d = s->yh[i] - s->ya[i]; ddy += d * d; }
+                    weight_update(s, sqrt(ddx), sqrt(ddy));
+                    memcpy(s->x, s->xh, sizeof(double) * n);
+                    memcpy(s->y, s->yh, sizeof(double) * m);
+                    memcpy(s->xa, s->xh, sizeof(double) * n);
+                    memcpy(s->ya, s->yh, sizeof(double) * m);
+                    s->t = 0;
+                    s->r_prev = INFINITY;
+                    s->restarts += 1;
+                } else {
+                    s->r_prev = r;
+                }
+            }
+        }
+        if (s->mode != MODE_NONE) {
+            if (s->k == P->max_iters) { s->status = 1; break; }
+            if (P->time_limit_s > 0.0 && now_s() - s->t0 > P->time_limit_s) { s->status = 2; break; }
+        }
+    }
+    return s->status;
+}
+
 /* Run up to `steps` more iterations (SURVEY §8(c) "loop"); returns status
  * (-1 = still running after `steps`). */
 int orc_run(orc_state *s, int64_t steps)
@@ -424,6 +548,7 @@ int orc_run(orc_state *s, int64_t steps)
     const orc_lp *lp = s->lp;
     int32_t m = lp->m, n = lp->n;
     const orc_params *P = &s->prm;
+    if (P->method == 1) return orc_run_halpern(s, steps);
     for (int64_t it = 0; it < steps && s->status < 0; ++it) {
         double tau = s->eta / s->omega;
         double sigma = s->eta * s->omega;
@@ -468,9 +593,7 @@ int orc_run(orc_state *s, int64_t steps)
                 double dx2 = 0.0, dy2 = 0.0;
                 for (int32_t j = 0; j < n; ++j) { double d = xc[j] - s->xr[j]; dx2 += d * d; }
                 for (int32_t i = 0; i < m; ++i) { double d = yc[i] - s->yr[i]; dy2 += d * d; }
-                double dx = sqrt(dx2), dy = sqrt(dy2);
-                if (dx > 1e-10 && dy > 1e-10)
-                    s->omega = exp(P->theta * log(dy / dx) + (1.0 - P->theta) * log(s->omega));
+                weight_update(s, sqrt(dx2), sqrt(dy2));
                 if (use_avg) {
                     memcpy(s->x, s->xavg, sizeof(double) * n);
                     memcpy(s->y, s->yavg, sizeof(double) * m);
@@ -501,8 +624,17 @@ void orc_get(const orc_state *s, double *x, double *y)
 {
     const double *xs = s->returned_average ? s->xavg : s->x;
     const double *ys = s->returned_average ? s->yavg : s->y;
+    if (s->prm.method == 1 && s->k > 0) { xs = s->xh; ys = s->yh; }   /* Halpern: T(z), the in-box point */
     if (x) memcpy(x, xs, sizeof(double) * s->lp->n);
     if (y) memcpy(y, ys, sizeof(double) * s->lp->m);
+}
+
+/* The internal iterate z = (x, y) (R-PDHG: the current iterate; Halpern: the Halpern
+ * sequence, which may leave the box) — test access for the Halpern pins. */
+void orc_get_z(const orc_state *s, double *x, double *y)
+{
+    if (x) memcpy(x, s->x, sizeof(double) * s->lp->n);
+    if (y) memcpy(y, s->y, sizeof(double) * s->lp->m);
 }
 
 void orc_result_of(orc_state *s, orc_result *r)

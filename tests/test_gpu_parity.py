@@ -266,14 +266,39 @@ def test_graph_and_eager_identical(problems):
     assert np.array_equal(xa, xb) and np.array_equal(ya, yb)   # deterministic reductions
 
 
-def test_trajectory(problems):
-    lp, olp, P = problems("c2-s")
+@pytest.mark.parametrize("name", ["c2-s", "c5-s"])
+def test_trajectory_matches_oracle(problems, name):
+    """Fig. 1 analogue: the steering phase's off-bound count (w.r.t. the
+    ORIGINAL bounds, tolerance eps_abs, S-10) and ||b - A x_k|| every 64 iterations.
+    The oracle runs the same Algorithm 1 model 64 iterations at a time in lockstep and
+    counts with its own orc_stats: counts bit-exact, residual norms to 1e-9."""
+    lp, olp, P = problems(name)
+    xo, yo, _ = oracle.solve(olp, oracle.default_params(max_iters=3000))
     S = cpd.Solver(P)
-    S.solve()
-    r, before, after = S.corner_push(candidate_floor=100)
+    S.set_iterate(xo, yo)
+    r, before, after = S.corner_push(seed=1001, candidate_floor=100, max_iters=5000)
     k, off, rp = S.trajectory()
-    assert len(k) == r["iterations"] // 64
-    assert np.all(np.diff(k) == 64) and np.all(off >= 0) and np.all(rp >= 0)
+    # oracle: Algorithm 1 line 2, then PDHG on M^ from (x*, 0), primal-only stop (P:391-395)
+    z = oracle.reduced_costs(olp, yo)
+    lh, uh, ch, _, _ = oracle.corner_model(olp, xo, z, 1e-6, 1.0, 1001)
+    p2 = oracle.default_params(max_iters=5000, primal_weight=0.0)
+    R = oracle.Run(olp, p2, c=ch, lb=lh, ub=uh, x_init=xo, y_init=None, mode=oracle.MODE_PRIMAL_ONLY,
+                   target=1e-4 * (1.0 + olp.nb), min_iters=100)
+    ko, offo, rpo = [], [], []
+    while True:
+        st = R.run(64 - R.k % 64)
+        if R.k % 64 == 0:
+            x, _ = R.get()
+            ko.append(R.k)
+            offo.append(oracle.stats(lp.m, x, None, lp.lb, lp.ub)["off_bound"])
+            rpo.append(float(np.linalg.norm(lp.b - olp.A_times(x))))
+        if st != -1:
+            break
+    assert r["iterations"] == R.k, (r["iterations"], R.k)
+    assert list(k) == ko
+    assert list(off) == offo, (list(off)[:8], offo[:8])
+    np.testing.assert_allclose(rp, rpo, rtol=1e-9, atol=1e-12)
+    assert off[0] <= before["off_bound"] + before["fix_lb"] + before["fix_ub"]
 
 
 @pytest.mark.parametrize("fmt", [("0", "0", "0"), ("1", "0", "0"), ("0", "1", "0"), ("1", "1", "0"),

@@ -15,7 +15,7 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PIN_TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_restart.py",
+PIN_TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_restart.py", "tests/test_oracle_halpern.py",
              "tests/test_oracle_scaling.py", "tests/test_oracle_ineq.py"]
 
 # (name, original text, mutated text) — each original must occur exactly once.
@@ -34,9 +34,12 @@ MUTATIONS = [
      "off_bound(x[j], l[j], uhat[j], eps_abs)"),
     ("zero_rc_strict", "fabs(z[j]) <= eps_abs;", "fabs(z[j]) < eps_abs;"),
     ("candidates_nonstrict", "off && fabs(z[j]) < eps_abs;", "off && fabs(z[j]) <= eps_abs;"),
-    ("omega_inverted", "log(dy / dx)", "log(dx / dy)"),
-    ("restart_every_check", "(double)s->t >= P->beta_art * (double)s->k",
-     "(double)s->t >= 0.0 * (double)s->k"),
+    ("omega_inverted", "exp(P->theta * log(dy / dx)", "exp(P->theta * log(dx / dy)"),
+    ("restart_every_check", "(S <= P->beta_nec * s->S_r && S > s->S_prev) ||\n                (double)s->t >= P->beta_art * (double)s->k",
+     "(S <= P->beta_nec * s->S_r && S > s->S_prev) ||\n                (double)s->t >= 0.0 * (double)s->k"),
+    ("halpern_restart_every_check", "(r <= P->beta_nec * s->r0 && r > s->r_prev) ||\n                    (double)s->t >= P->beta_art * (double)s->k",
+     "(r <= P->beta_nec * s->r0 && r > s->r_prev) ||\n                    (double)s->t >= 0.0 * (double)s->k"),
+    ("halpern_r0_every_iter", "if (s->t == 0) s->r0 = r;", "s->r0 = r;"),
     ("sufficient_off", "if (S <= P->beta_suff * s->S_r ||", "if (0 ||"),
     ("no_S_prev_reset", "s->S_prev = INFINITY;\n                s->t = 0;", "s->t = 0;"),
     ("upper_term_sign", "bound_terms -= u[j] * zm;", "bound_terms += u[j] * zm;"),
@@ -44,6 +47,19 @@ MUTATIONS = [
     ("extrapolation_dropped", "s->xbar[j] = 2.0 * s->xn[j] - s->x[j];", "s->xbar[j] = s->xn[j];"),
     ("bound_map_nonstrict", "if (z[j] < -eps_abs) { lhat[j] = x[j];", "if (z[j] <= -eps_abs) { lhat[j] = x[j];"),
     ("est_dual_from_off", "(m > st->zero_rc ? m - st->zero_rc : 0)", "(m > st->off_bound ? m - st->off_bound : 0)"),
+    # reflected restarted Halpern PDHG + PID weight (NEXT-1)
+    ("halpern_lambda", "double lam = (double)(s->t + 1) / (double)(s->t + 2);",
+     "double lam = (double)(s->t + 1) / (double)(s->t + 3);"),
+    ("halpern_no_reflection", "s->x[j] = lam * ((1.0 + rho) * s->xh[j] - rho * s->x[j])",
+     "s->x[j] = lam * (s->xh[j])"),
+    ("halpern_anchor_dropped", "+ (1.0 - lam) * s->ya[i];", "+ (1.0 - lam) * s->y[i];"),
+    ("halpern_cross_sign", "double r2 = dx2 / tau + dy2 / sigma + 2.0 * cross;",
+     "double r2 = dx2 / tau + dy2 / sigma - 2.0 * cross;"),
+    ("halpern_restart_to_z", "memcpy(s->x, s->xh, sizeof(double) * n);\n                    memcpy(s->y, s->yh",
+     "memcpy(s->xh, s->x, sizeof(double) * n);\n                    memcpy(s->y, s->yh"),
+    ("halpern_returns_z", "if (s->prm.method == 1 && s->k > 0) { xs = s->xh; ys = s->yh; }", ""),
+    ("pid_integral_dropped", "+ P->ki * s->pid_int", "+ P->ki * e"),
+    ("pid_derivative_sign", "P->kd * (e - s->pid_eprev)", "P->kd * (s->pid_eprev - e)"),
 ]
 
 
