@@ -116,6 +116,14 @@ typedef struct {
     double beta_suff, beta_nec, beta_art, theta;   /* 0.2, 0.8, 0.36, 0.5 */
     int32_t use_graph;     /* 1: CUDA-graph batches of K iterations (default); 0: eager launches */
     int32_t profile;       /* 1: CUDA events around every hot kernel (cpd_get_kernel_times) */
+    /* NEXT-1 (the cuPDLP+ lineage of the paper's PDHG; readings H-1..H-4) */
+    int32_t method;        /* 0: R-PDHG (restart to average / current); 1: reflected restarted
+                              Halpern PDHG: z+ = l((1+reflection) T(z) - reflection z) + (1-l) z_anchor,
+                              l = (t+1)/(t+2), restarts on the fixed-point residual ||z - T(z)||_M,
+                              termination and the returned point are those of T(z) (single GPU only) */
+    double reflection;     /* 1.0 */
+    int32_t pid;           /* 1: PID primal weight at restarts on e = log(dy/dx) - log omega */
+    double kp, ki, kd;     /* 0.99, 0.01, 0: PID gains (log omega += kp e + ki sum e + kd (e - e_prev)) */
 } cpd_params;
 void cpd_params_default(cpd_params *p);
 

@@ -49,7 +49,9 @@ class Params(C.Structure):
                 ("step_size", C.c_double), ("power_iters", C.c_int32), ("seed", C.c_uint64),
                 ("primal_weight", C.c_double), ("restart", C.c_int32), ("beta_suff", C.c_double),
                 ("beta_nec", C.c_double), ("beta_art", C.c_double), ("theta", C.c_double),
-                ("use_graph", C.c_int32), ("profile", C.c_int32)]
+                ("use_graph", C.c_int32), ("profile", C.c_int32),
+                ("method", C.c_int32), ("reflection", C.c_double), ("pid", C.c_int32),
+                ("kp", C.c_double), ("ki", C.c_double), ("kd", C.c_double)]
 
 
 class Result(C.Structure):

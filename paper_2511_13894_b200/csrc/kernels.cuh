@@ -146,7 +146,30 @@ struct Ctl {
     double* traj_rp;
     // generic totals written by one-off kernels (norms, stats, score)
     double out[NSMAX];
+    // reflected restarted Halpern PDHG + PID primal weight (NEXT-1; H-1..H-4)
+    int32_t method, pid;
+    double rho, kp, ki, kd;
+    double r0, r_prev, r_last;          // fixed-point residuals: at the anchor, last check, last iteration
+    double pid_int, pid_eprev;
+    double dx2_h, dxa2_h, dya2_h;       // ||xh - x||^2, ||xh - x_anchor||^2, ||yh - y_anchor||^2 (last iteration)
+    double rp2_h, bty_h;                // ||b - A xh||^2, b^T yh of the last T(z)
 };
+
+// Primal-weight update at a restart from the anchor movement (dx, dy): theta smoothing
+// (R-PDHG, S-1) or the PID controller on e = log(dy/dx) - log omega (reading H-3).
+__device__ __forceinline__ void weight_update(Ctl* ctl, double dx, double dy)
+{
+    if (!(dx > 1e-10 && dy > 1e-10)) return;
+    if (ctl->pid) {
+        const double e = log(dy / dx) - log(ctl->omega);
+        ctl->pid_int += e;
+        const double lw = log(ctl->omega) + ctl->kp * e + ctl->ki * ctl->pid_int + ctl->kd * (e - ctl->pid_eprev);
+        ctl->pid_eprev = e;
+        ctl->omega = exp(lw);
+    } else {
+        ctl->omega = exp(ctl->theta * log(dy / dx) + (1.0 - ctl->theta) * log(ctl->omega));
+    }
+}
 
 struct Gate {
     int32_t kind, slot, node;
@@ -1761,8 +1784,7 @@ struct EpiCheckM {
                 (double)ctl->t >= ctl->beta_art * (double)k) {
                 const double dx = sqrt(use_avg ? en[7] : en[3]);
                 const double dy = sqrt(use_avg ? tot[3] : tot[2]);
-                if (dx > 1e-10 && dy > 1e-10)
-                    ctl->omega = exp(ctl->theta * log(dy / dx) + (1.0 - ctl->theta) * log(ctl->omega));
+                weight_update(ctl, dx, dy);
                 ctl->tau = ctl->eta / ctl->omega;
                 ctl->sigma = ctl->eta * ctl->omega;
                 if (use_avg) {
@@ -1783,6 +1805,227 @@ struct EpiCheckM {
             ctl->done = 1; ctl->status = ST_ITER_LIMIT; ctl->iterations = k;
         }
     }
+};
+
+// ------------------------------------------------------------ reflected restarted Halpern PDHG
+// (the cuPDLP+ lineage of P:412-414; readings H-1..H-4).
+// z = (x, y) is the Halpern sequence, zh = T(z) the PDHG map's output (the in-box point
+// every test is made on and the point a run returns), z_a the anchor, t the iterations
+// since the last restart, lambda = (t+1)/(t+2):
+//   K1: xh = proj(x - tau (c - A^T y));  x+ = lambda((1+rho) xh - rho x) + (1-lambda) x_a
+//   K2: yh = y + sigma (b - (2 A xh - A x));  y+ = lambda((1+rho) yh - rho y) + (1-lambda) y_a
+//       A x+ = lambda((1+rho) A xh - rho A x) + (1-lambda) A x_a   (kept per row: no extra SpMV)
+//       r^2 = ||xh-x||^2/tau + ||yh-y||^2/sigma + 2 <yh-y, A xh - A x>   (fixed-point residual)
+//   every K: score(zh) (one A^T pass over yh), restart on r, weight from the anchor movement.
+
+// K1: staged per-row inputs 0 c, 1 x_k, 2 x_anchor (3 lb, 4 ub with per-element bounds).
+template <bool PE>
+struct EpiPrimalH {
+    static constexpr int NS = 3;   // ||xh - x||^2, ||xh - x_a||^2, #nonfinite(xh)
+    static constexpr int NVEC = PE ? 5 : 3;
+    const double* c;
+    Bounds bd;
+    PingPong X;
+    const double* xa;
+    double* xh;
+    double tau, lam, rho;
+    const double* xc;
+    double* xn;
+    __device__ void load(const Ctl* ctl)
+    {
+        tau = ctl->tau;
+        rho = ctl->rho;
+        lam = (double)(ctl->t + 1) / (double)(ctl->t + 2);
+        xc = X.at(ctl->k);
+        xn = X.at(ctl->k + 1);
+    }
+    __device__ __forceinline__ const double* vec(int v) const
+    {
+        return v == 0 ? c : v == 1 ? xc : v == 2 ? xa : v == 3 ? bd.l : bd.u;
+    }
+    __device__ __forceinline__ void row(int j, const double* s, const double* const* vin, int li,
+                                        double* acc) const
+    {
+        const double x = vin[1][li];
+        double lo = bd.l0, hi = bd.u0;
+        if constexpr (PE) {
+            lo = vin[3][li];
+            hi = vin[4][li];
+        }
+        const double h = proj(x - tau * (vin[0][li] - s[0]), lo, hi);
+        st_keep(&xh[j], h);   // gathered by the dual step
+        const double a = vin[2][li];
+        __stcs(&xn[j], lam * ((1.0 + rho) * h - rho * x) + (1.0 - lam) * a);
+        acc[0] += (h - x) * (h - x);
+        acc[1] += (h - a) * (h - a);
+        acc[2] += isfinite(h) ? 0.0 : 1.0;
+    }
+    __device__ void finalize(const double* tot, Ctl* ctl) const
+    {
+        ctl->restart_flag = 0;
+        ctl->dx2_h = tot[0];
+        ctl->dxa2_h = tot[1];
+        ctl->nonfinite_x = tot[2] > 0.0;
+    }
+};
+
+// K2: staged per-row inputs 0 b, 1 y_k, 2 (A x_k), 3 y_anchor, 4 (A x_anchor).
+struct EpiDualH {
+    static constexpr int NS = 6;   // ||b - A xh||^2, b^T yh, ||yh - y||^2, <yh - y, A xh - A x>, ||yh - y_a||^2, #nonfinite
+    static constexpr int NVEC = 5;
+    const double* b;
+    double *y, *ax, *yh, *axh;
+    const double *ya, *axa;
+    double sigma, lam, rho;
+    const double* w = nullptr;   // 1/r (scaled problem): ||r_P|| in the original space
+    const int8_t* sn = nullptr;
+    __device__ void load(const Ctl* ctl)
+    {
+        sigma = ctl->sigma;
+        rho = ctl->rho;
+        lam = (double)(ctl->t + 1) / (double)(ctl->t + 2);
+    }
+    __device__ __forceinline__ const double* vec(int v) const
+    {
+        return v == 0 ? b : v == 1 ? y : v == 2 ? ax : v == 3 ? ya : axa;
+    }
+    __device__ __forceinline__ void row(int i, const double* s, const double* const* vin, int li,
+                                        double* acc) const
+    {
+        const double sh = s[0];   // (A xh)_i
+        const double bi = vin[0][li], yo = vin[1][li], axo = vin[2][li];
+        const double h = dual_proj(sn, i, yo + sigma * (bi - (2.0 * sh - axo)));
+        y[i] = lam * ((1.0 + rho) * h - rho * yo) + (1.0 - lam) * vin[3][li];
+        ax[i] = lam * ((1.0 + rho) * sh - rho * axo) + (1.0 - lam) * vin[4][li];
+        yh[i] = h;
+        axh[i] = sh;
+        const double r = row_viol(sn, i, bi - sh) * (w ? w[i] : 1.0);
+        acc[0] += r * r;
+        acc[1] += bi * h;
+        acc[2] += (h - yo) * (h - yo);
+        acc[3] += (h - yo) * (sh - axo);
+        acc[4] += (h - vin[3][li]) * (h - vin[3][li]);
+        acc[5] += isfinite(h) ? 0.0 : 1.0;
+    }
+    __device__ void finalize(const double* tot, Ctl* ctl) const
+    {
+        if (tot[5] > 0.0 || ctl->nonfinite_x) {
+            ctl->done = 1; ctl->status = ST_FAIL; ctl->iterations = ctl->k + 1;
+            return;
+        }
+        const double r2 = ctl->dx2_h / ctl->tau + tot[2] / ctl->sigma + 2.0 * tot[3];
+        const double r = sqrt(r2 > 0.0 ? r2 : 0.0);
+        if (ctl->t == 0) ctl->r0 = r;   // the residual at the anchor
+        ctl->r_last = r;
+        ctl->rp2_h = tot[0];
+        ctl->bty_h = tot[1];
+        ctl->dya2_h = tot[4];
+        ctl->k += 1;
+        ctl->t += 1;
+        const int64_t k = ctl->k;
+        if (ctl->mode == MODE_PRIMAL_ONLY && k >= ctl->min_iters && sqrt(tot[0]) <= ctl->target) {
+            ctl->done = 1; ctl->status = ST_CONVERGED; ctl->iterations = k;
+            return;
+        }
+        if ((k % ctl->K) == 0 && (ctl->restart_on || ctl->mode != MODE_NONE)) {
+            ctl->check_pending = 1;
+        } else if (ctl->mode != MODE_NONE && k == ctl->max_iters) {
+            ctl->done = 1; ctl->status = ST_ITER_LIMIT; ctl->iterations = k;
+        }
+    }
+};
+
+// Check of a Halpern run (every K): A^T yh -> score(zh), trajectory, restart
+// on the fixed-point residual, weight update from the anchor movement.
+struct EpiCheckH {
+    static constexpr int NS = 4;   // c^T xh, ||r_D(yh)||^2, bound terms, off-bound(xh; M)
+    static constexpr int NVEC = 0;
+    __device__ __forceinline__ const double* vec(int) const { return nullptr; }
+    const double* c;
+    const double* xh;
+    Bounds bd, orig;
+    double eps_abs;
+    int traj;
+    const double* w = nullptr;    // 1/s (scaled problem)
+    const double* sx = nullptr;   // s: the trajectory count tests x = s x^ against orig
+    __device__ void load(const Ctl* ctl)
+    {
+        traj = ctl->traj_on;
+        eps_abs = ctl->eps_abs;
+    }
+    __device__ __forceinline__ void row(int j, const double* s, const double* const*, int, double* acc) const
+    {
+        const double cj = c[j], x = xh[j];
+        acc[0] += cj * x;
+        dual_terms(cj - s[0], bd.lo(j), bd.hi(j), acc[1], acc[2], w ? w[j] : 1.0);
+        if (traj) {
+            const double xo = sx ? x * sx[j] : x;
+            acc[3] += ((xo - orig.lo(j) > eps_abs) && (orig.hi(j) - xo > eps_abs)) ? 1.0 : 0.0;
+        }
+    }
+    __device__ void finalize(const double* tot, Ctl* ctl) const
+    {
+        const int64_t k = ctl->k;
+        double o[8];
+        score8(ctl->rp2_h, tot[1], tot[0], ctl->bty_h + tot[2], ctl->nb, ctl->nc, o);
+        for (int i = 0; i < 8; ++i) ctl->last[i] = o[i];
+        if (ctl->traj_on && ctl->traj_len < ctl->traj_cap) {
+            ctl->traj_k[ctl->traj_len] = k;
+            ctl->traj_off[ctl->traj_len] = (int64_t)tot[3];
+            ctl->traj_rp[ctl->traj_len] = o[0];
+            ctl->traj_len += 1;
+        }
+        ctl->check_pending = 0;
+        if (ctl->mode == MODE_FULL && o[7] <= ctl->eps_rel) {
+            ctl->done = 1; ctl->status = ST_CONVERGED; ctl->iterations = k;
+            return;
+        }
+        if (ctl->restart_on) {
+            const double r = ctl->r_last;
+            if (r <= ctl->beta_suff * ctl->r0 || (r <= ctl->beta_nec * ctl->r0 && r > ctl->r_prev) ||
+                (double)ctl->t >= ctl->beta_art * (double)k) {
+                weight_update(ctl, sqrt(ctl->dxa2_h), sqrt(ctl->dya2_h));
+                ctl->tau = ctl->eta / ctl->omega;
+                ctl->sigma = ctl->eta * ctl->omega;
+                ctl->restart_flag = 1;
+                ctl->r_prev = INFINITY;
+                ctl->t = 0;
+                ctl->restarts += 1;
+            } else {
+                ctl->r_prev = r;
+            }
+        }
+        if (ctl->mode != MODE_NONE && k == ctl->max_iters) {
+            ctl->done = 1; ctl->status = ST_ITER_LIMIT; ctl->iterations = k;
+        }
+    }
+};
+
+// Halpern restart apply: z = z_anchor = zh (and their A x), the iterate of k.
+struct OpRestartH {
+    static constexpr int NS = 1;
+    PingPong X;
+    double *xa, *y, *ya, *ax, *axa;
+    const double *xh, *yh, *axh;
+    int32_t n, m;
+    double* xc;
+    __device__ void load(const Ctl* ctl) { xc = X.at(ctl->k); }
+    __device__ __forceinline__ void elem(int64_t i, double*) const
+    {
+        if (i < n) {
+            const double v = xh[i];
+            xc[i] = v;
+            xa[i] = v;
+        }
+        if (i < m) {
+            const double v = yh[i], a = axh[i];
+            y[i] = v;
+            ya[i] = v;
+            ax[i] = a;
+            axa[i] = a;
+        }
+    }
+    __device__ void finalize(const double*, Ctl*) const {}
 };
 
 // Restart apply: (x, y, Ax) <- candidate; (x_r, y_r) <- (x, y); averages <- 0.

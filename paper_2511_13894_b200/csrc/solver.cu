@@ -603,6 +603,7 @@ struct cpd_solver {
     // state vectors: n-side (x-like) of length own_len[1], m-side (y-like) own_len[0]
     DBuf<double> X0, X1, Xa0, Xa1, Xr, Y, Ya, Yr, AX, AXa, Ystar, Z, lhat, uhat, chat, objd, SN, SM;
     DBuf<double> LHo, UHo, TX, TY, TY2;   // scaled problems: original-space model bounds; unscale scratch
+    DBuf<double> XH, YH, AXH;         // Halpern: T(z) = (xh, yh) of the last iteration and A xh
     DBuf<int8_t> shat;                // corner-model row senses
     DBuf<double> ACC;                 // short-row push sums (m), zero between iterations
     int64_t rows_eq = 0;
@@ -638,6 +639,11 @@ struct cpd_solver {
         for (auto* b : {&Y, &Ya, &Yr, &AX, &AXa, &Ystar, &SM}) b->alloc(m);
         for (auto* b : {&X0, &X1, &Xa0, &Xa1, &Xr, &Z}) CPD_CUDA(cudaMemset(b->p, 0, sizeof(double) * n));
         for (auto* b : {&Y, &Ya, &Yr, &AX, &AXa, &Ystar}) CPD_CUDA(cudaMemset(b->p, 0, sizeof(double) * m));
+        if (pr.method == 1) {
+            XH.alloc(n);
+            YH.alloc(m);
+            AXH.alloc(m);
+        }
         if (p->push_on) {
             ACC.alloc(std::max<int32_t>(p->m, 1));
             CPD_CUDA(cudaMemset(ACC.p, 0, sizeof(double) * p->m));
@@ -716,6 +722,13 @@ struct cpd_solver {
         h.traj_k = trk.p;
         h.traj_off = troff.p;
         h.traj_rp = trrp.p;
+        h.method = prm.method;
+        h.pid = prm.pid;
+        h.rho = prm.reflection;
+        h.kp = prm.kp;
+        h.ki = prm.ki;
+        h.kd = prm.kd;
+        h.r0 = h.r_prev = h.r_last = INFINITY;
         cx.push_ctl(h);
         if (ACC.p) CPD_CUDA(cudaMemsetAsync(ACC.p, 0, sizeof(double) * P->m, cx.st));   // no stale pushes
         Reps rp(P, RV.p);
@@ -737,12 +750,68 @@ struct cpd_solver {
         // the batch's K1 gathers the y replica: refresh it here (split m-side)
         refresh(cx, 0, fixed(Y.p), RV.p, always());
         pass<1>(cx, 1, gsrc(0, fixed(Y.p), RV.p), none(), en, always());
+        if (prm.method == 1) {   // Halpern: anchor z_a = z_0 (and A x_a), T(z) "so far" = z_0
+            const int g = std::min<int64_t>(cx.grid_elem, ((int64_t)std::max(n, m) + 255) / 256 + 1);
+            k_copy<<<g, 256, 0, cx.st>>>(n, Xa0.p, X0.p);
+            k_copy<<<g, 256, 0, cx.st>>>(n, XH.p, X0.p);
+            k_copy<<<g, 256, 0, cx.st>>>(m, Ya.p, Y.p);
+            k_copy<<<g, 256, 0, cx.st>>>(m, YH.p, Y.p);
+            k_copy<<<g, 256, 0, cx.st>>>(m, AXa.p, AX.p);
+            k_copy<<<g, 256, 0, cx.st>>>(m, AXH.p, AX.p);
+            CPD_CUDA(cudaGetLastError());
+            cx.launches += 6;
+        }
         cx.pull_ctl();
         cur_par = 0;
         run_active = true;
         run_kind = rc.kind;
         if (!std::isfinite(cx.h_ctl->eta) || !(cx.h_ctl->eta > 0.0))
             throw Error(CPD_E_ARG, "step size is not positive and finite (zero matrix?)");
+    }
+
+    // ---------------------------------------------------------- one Halpern batch
+    // [check: A^T yh -> score(zh), restart test] [restart apply] (K1_s, K2_s)_{s<K}
+    template <class Rec>
+    void enqueue_batch_halpern(int kind, bool, Rec& rec)
+    {
+        const int32_t n = nO(), m = mO();
+        const int K = prm.check_every;
+        const double* c = obj_of(kind);
+        const Bounds bd = bounds_of(kind);
+        const PingPong X{{X0.p, X1.p}};
+        {
+            EpiCheckH e{c, XH.p, bd, P->bounds_orig(), 0.0, 0};
+            e.w = P->w_n();
+            e.sx = P->s_n();
+            Gate g{GATE_CHECK, 0, NODE_CHECK_N, active.p};
+            rec(ev0, NODE_CHECK_N);
+            pass<1>(cx, 1, fixed(YH.p), none(), e, g);
+            rec(ev1, NODE_CHECK_N);
+            OpRestartH orr{X, Xa0.p, Y.p, Ya.p, AX.p, AXa.p, XH.p, YH.p, AXH.p, n, m, nullptr};
+            Gate gr{GATE_RESTART, 0, NODE_RESTART, active.p};
+            rec(ev0, NODE_RESTART);
+            elem(cx, std::max(n, m), orr, gr, false);
+            rec(ev1, NODE_RESTART);
+        }
+        for (int s = 0; s < K; ++s) {
+            const int n1 = NODE_K0 + 2 * s, n2 = n1 + 1;
+            const Gate g1{GATE_K1, s, n1, active.p}, g2{GATE_K2, s, n2, active.p};
+            rec(ev0, n1);
+            if (kind == 0 && P->uniform_bounds) {
+                EpiPrimalH<false> e1{c, bd, X, Xa0.p, XH.p, 0.0, 0.0, 0.0, nullptr, nullptr};
+                pass<1>(cx, 1, fixed(Y.p), none(), e1, g1);
+            } else {
+                EpiPrimalH<true> e1{c, bd, X, Xa0.p, XH.p, 0.0, 0.0, 0.0, nullptr, nullptr};
+                pass<1>(cx, 1, fixed(Y.p), none(), e1, g1);
+            }
+            rec(ev1, n1);
+            EpiDualH e2{P->b_own(), Y.p, AX.p, YH.p, AXH.p, Ya.p, AXa.p, 0.0, 0.0, 0.0};
+            e2.w = P->w_m();
+            e2.sn = sense_of(kind);
+            rec(ev0, n2);
+            pass<1>(cx, 0, fixed(XH.p), none(), e2, g2);
+            rec(ev1, n2);
+        }
     }
 
     // ---------------------------------------------------------- one batch
@@ -761,6 +830,13 @@ struct cpd_solver {
             else CPD_CUDA(cudaEventRecord(ev[node], cx.st));
         };
         CPD_CUDA(cudaMemsetAsync(active.p, 0, sizeof(int32_t) * nnodes, cx.st));
+        if (prm.method == 1) {   // reflected restarted Halpern PDHG (NEXT-1)
+            enqueue_batch_halpern(kind, capture, rec);
+            if (capture) graph_kernels[kind] = cx.launches - l0;
+            CPD_CUDA(cudaMemcpyAsync(h_active, active.p, sizeof(int32_t) * nnodes, cudaMemcpyDeviceToHost, cx.st));
+            CPD_CUDA(cudaMemcpyAsync(cx.h_ctl, cx.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, cx.st));
+            return;
+        }
         // restart check: A^T pass (current y and average y) + A pass (A x_avg) + decision
         {
             EpiCheckN e{c, bd, orig, X, Xa, Xr.p, prm.restart ? 1 : 0, 0.0, nullptr, nullptr, 0};
@@ -901,7 +977,13 @@ struct cpd_solver {
         const Ctl& h = *cx.h_ctl;
         const int64_t k = h.k;
         cur_par = (int)(k & 1);
-        if (h.returned_average) {
+        if (prm.method == 1 && k > 0) {   // Halpern: the run returns T(z) of its last iteration
+            const int g = std::min<int64_t>(cx.grid_elem, ((int64_t)std::max(nO(), mO()) + 255) / 256 + 1);
+            k_copy<<<g, 256, 0, cx.st>>>(nO(), Xp(cur_par), XH.p);
+            k_copy<<<g, 256, 0, cx.st>>>(mO(), Y.p, YH.p);
+            CPD_CUDA(cudaGetLastError());
+            cx.launches += 2;
+        } else if (h.returned_average) {
             const int g = std::min<int64_t>(cx.grid_elem, ((int64_t)std::max(nO(), mO()) + 255) / 256 + 1);
             k_copy<<<g, 256, 0, cx.st>>>(nO(), Xp(cur_par), (k & 1) ? Xa1.p : Xa0.p);
             k_copy<<<g, 256, 0, cx.st>>>(mO(), Y.p, Ya.p);
@@ -1195,6 +1277,16 @@ struct cpd_solver {
         // short-row push: their entries are read again by K1 (12 B) and not by K2; K2
         // reads and zeroes acc (16 B per row)
         const double pz = P->push_on ? (double)P->push_nnz : 0.0;
+        if (prm.method == 1) {
+            // Halpern: K1 reads c, x, x_anchor, writes xh, x+ (40 B per column, as R-PDHG);
+            // K2 reads b, y, Ax, y_anchor, Ax_anchor and writes y+, Ax+, yh, A xh (72 B per row);
+            // the check is one A^T pass over yh reading c, xh; restart copies 3 n- and 6 m-vectors
+            if (base == "primal_step_AT") return 12 * nnz + 4 * (nr + 1) + 8 * mr + 40 * n + bnd;
+            if (base == "dual_step_A") return 12 * nnz + 4 * (mr + 1) + 8 * nr + 72 * m;
+            if (base == "check_eval_AT") return 12 * nnz + 4 * (nr + 1) + 8 * mr + 16 * n + bnd;
+            if (base == "restart_apply") return 24 * n + 48 * m;
+            return -1.0;
+        }
         if (base == "primal_step_AT") return 12 * nnz + 4 * (nr + 1) + 8 * mr + 40 * n + bnd + 12 * pz;
         if (base == "dual_step_A")
             return 12 * (nnz - pz) + 4 * (mr + 1) + 8 * nr + 56 * m + (P->push_on ? 16.0 * mr : 0.0);
@@ -1403,6 +1495,12 @@ void cpd_params_default(cpd_params* p)
     p->theta = 0.5;
     p->use_graph = 1;
     p->profile = 0;
+    p->method = 0;
+    p->reflection = 1.0;
+    p->pid = 0;
+    p->kp = 0.99;
+    p->ki = 0.01;
+    p->kd = 0.0;
 }
 
 void cpd_corner_params_default(cpd_corner_params* p)
@@ -1430,8 +1528,11 @@ int cpd_solver_create(const cpd_problem* p, const cpd_params* prm, cpd_solver** 
     const cpd_params& pr = prm ? *prm : d;
     if (pr.check_every < 1 || pr.check_every > 1024) return fail(CPD_E_ARG, "check_every must be in [1, 1024]");
     if (!(pr.eps_rel > 0.0) || !(pr.step_scale > 0.0) || pr.power_iters < 1 || pr.max_iters < 0 ||
-        pr.restart < 0 || pr.restart > 1)
+        pr.restart < 0 || pr.restart > 1 || pr.method < 0 || pr.method > 1 || !(pr.reflection >= 0.0) ||
+        pr.pid < 0 || pr.pid > 1 || !std::isfinite(pr.kp) || !std::isfinite(pr.ki) || !std::isfinite(pr.kd))
         return fail(CPD_E_ARG, "invalid parameter");
+    if (pr.method == 1 && p->split >= 0)
+        return fail(CPD_E_ARG, "the Halpern method (method = 1) is single-GPU only");
     CPD_CUDA(cudaSetDevice(p->device));
     *out = new cpd_solver(p, pr);
     p->live_solvers.fetch_add(1);
