@@ -24,7 +24,7 @@ CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-std=c11", "-fPIC", "-s
 _lock = threading.Lock()
 _lib = None
 
-MODE_FULL, MODE_PRIMAL_ONLY, MODE_NONE = 0, 1, 2
+MODE_FULL, MODE_PRIMAL_ONLY, MODE_NONE, MODE_DUAL_ONLY = 0, 1, 2, 3
 STATUS = {0: "converged", 1: "iter_limit", 2: "time_limit", 3: "numerical_failure", -1: "running"}
 
 
@@ -121,6 +121,7 @@ def lib():
             L.orc_stats.argtypes = [C.c_int32, C.c_int32, P, P, P, P, P, P, C.c_double,
                                     C.c_int64, C.POINTER(Stats)]
             L.orc_scale.argtypes = [C.c_int32, C.c_int32, P, P, P, C.c_int32, C.c_int32, P, P]
+            L.orc_dual_corner_model.argtypes = [C.c_int32, P, P, P, C.c_double, P, P, P]
             L.orc_corner_senses.restype = C.c_int64
             L.orc_corner_senses.argtypes = [C.c_int32, P, P, C.c_double, P]
             L.orc_set_original.argtypes = [P, C.POINTER(LPStruct), P, P, P, P, P]
@@ -172,6 +173,16 @@ class OracleLP:
         self.s = LPStruct(self.m, self.n, _p(self.Ap), _p(self.Aj), _p(self.Ax),
                           _p(self.ATp), _p(self.ATj), _p(self.ATx), _p(self.b), _p(self.sense))
         self.nb = float(L.orc_norm2(self.m, _p(self.b)))
+
+    def with_b(self, b):
+        """The same LP with another right-hand side (shares every other array)."""
+        import copy
+        o = copy.copy(self)
+        o.b = _f64(b).copy()
+        o.s = LPStruct(self.m, self.n, _p(self.Ap), _p(self.Aj), _p(self.Ax),
+                       _p(self.ATp), _p(self.ATj), _p(self.ATx), _p(o.b), _p(self.sense))
+        o.nb = float(lib().orc_norm2(self.m, _p(o.b)))
+        return o
 
     def with_senses(self, sense):
         """The same LP with other row senses (shares every array)."""
@@ -434,3 +445,44 @@ def corner_push(olp: OracleLP, x, y, params: Params = None, eps_abs=1e-6, obj_sc
     before["fix_ub"] = after["fix_ub"] = fu
     return xh, y, z, res, before, after, dict(lhat=lh, uhat=uh, chat=ch, target=target, shat=shat,
                                               rows_eq=nrows_eq)
+
+
+def dual_corner_model(olp: OracleLP, x, eps_abs=1e-6):
+    """NEXT-4 dual corner model bounds (orc_dual_corner_model): (lhat, uhat, class counts)."""
+    x = _f64(x)
+    lh, uh = np.zeros(olp.n), np.zeros(olp.n)
+    cnt = np.zeros(3, np.int64)
+    lib().orc_dual_corner_model(olp.n, _p(x), _p(olp.lb), _p(olp.ub), eps_abs, _p(lh), _p(uh), _p(cnt))
+    return lh, uh, dict(off=int(cnt[0]), lower=int(cnt[1]), upper=int(cnt[2]))
+
+
+def dual_corner_push(olp: OracleLP, x, y, params: Params = None, eps_abs=1e-6, min_iters=100,
+                     max_iters=100000, eta=0.0, floor=100_000):
+    """NEXT-4 (D-1..D-4): PDHG on the dual corner model (A, b, c, lhat, uhat) from
+    (x, y), stopped at k >= min_iters once every column's dual violation is <= eps_abs
+    (D-3).  Returns (x, yhat, zhat, result, stats_before, stats_after, model): x is phase
+    1's; d = #{|z_j| <= eps_abs} and the dual-push estimate m - d before / after."""
+    params = params or default_params()
+    lh, uh, cnt = dual_corner_model(olp, x, eps_abs)
+    z0 = reduced_costs(olp, y)
+    before = stats(olp.m, x, z0, olp.lb, olp.ub, None, None, eps_abs, floor)
+    p2 = default_params(**{k: getattr(params, k) for k, _ in Params._fields_})
+    p2.max_iters = max_iters
+    p2.primal_weight = 0.0
+    p2.eps_abs = eps_abs
+    r = Run(olp, p2, c=olp.c, lb=lh, ub=uh, x_init=x, y_init=y, mode=MODE_DUAL_ONLY, target=0.0,
+            min_iters=min_iters, eta=eta)
+    r.run(np.iinfo(np.int64).max)
+    _, yh = r.get()
+    res = r.result()
+    zh = reduced_costs(olp, yh)
+    after = stats(olp.m, x, zh, olp.lb, olp.ub, None, None, eps_abs, floor)
+    return _f64(x), yh, zh, res, before, after, dict(lhat=lh, uhat=uh, **cnt)
+
+
+def corner_decide(st: dict, m: int):
+    """On-the-fly choice of the push phases from the phase-1 statistics (NEXT-4, P:200-210,
+    P:438-452; reading D-4): (primal, dual) booleans."""
+    primal = bool(st["is_candidate"])
+    dual = st["est_dual_pushes"] > 0 and min(m, st["off_bound"]) > st["zero_rc"]
+    return primal, dual

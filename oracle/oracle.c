@@ -79,7 +79,7 @@ typedef struct {
     int32_t is_candidate;
 } orc_stats_t;
 
-enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2 };
+enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2, MODE_DUAL_ONLY = 3 };
 
 /* ---------------------------------------------------------- basic helpers */
 
@@ -436,6 +436,23 @@ static double primal_res(orc_state *s, const double *x)
     return sqrt(r2);
 }
 
+/* Number of columns whose dual violation r_D_j (S-6, w.r.t. the run's bounds) exceeds
+ * eps_abs in absolute value: the dual corner push stops when it is 0 (reading D-3). */
+static int64_t dual_viol_count(orc_state *s, const double *y)
+{
+    const orc_lp *lp = s->lp;
+    orc_spmv(lp->n, lp->ATp, lp->ATj, lp->ATx, y, s->aty);
+    int64_t cnt = 0;
+    for (int32_t j = 0; j < lp->n; ++j) {
+        double z = s->c[j] - s->aty[j];
+        double zp = z > 0.0 ? z : 0.0, zm = -z > 0.0 ? -z : 0.0, rd = z;
+        if (s->l[j] > -INFINITY) rd -= zp;
+        if (s->u[j] < INFINITY) rd += zm;
+        cnt += fabs(rd) > s->prm.eps_abs;
+    }
+    return cnt;
+}
+
 /* Primal-weight update at a restart from the anchor movement (dx, dy): theta
  * smoothing (S-1, PDLP lineage) or, with pid, a PID controller on the log-ratio error
  * e = log(dy/dx) - log omega (reading H-3):
@@ -514,6 +531,9 @@ static int orc_run_halpern(orc_state *s, int64_t steps)
         if (s->t % P->check_every == 0) {
             double S = score_of(s, s->xh, s->yh, &o);
             if (s->mode == MODE_FULL && S <= P->eps_rel) { s->status = 0; break; }
+            if (s->mode == MODE_DUAL_ONLY && s->k >= s->min_iters && dual_viol_count(s, s->yh) == 0) {
+                s->status = 0; break;
+            }
             if (P->restart) {
                 if (r <= P->beta_suff * s->r0 || (r <= P->beta_nec * s->r0 && r > s->r_prev) ||
                     (double)s->t >= P->beta_art * (double)s->k) {
@@ -576,6 +596,8 @@ int orc_run(orc_state *s, int64_t steps)
             if (score_of(s, s->x, s->y, &o) <= P->eps_rel) { s->status = 0; break; }
         } else if (s->mode == MODE_PRIMAL_ONLY) {
             if (s->k >= s->min_iters && primal_res(s, s->x) <= s->target) { s->status = 0; break; }
+        } else if (s->mode == MODE_DUAL_ONLY) {   /* dual corner push stop (NEXT-4, reading D-3) */
+            if (s->k >= s->min_iters && dual_viol_count(s, s->y) == 0) { s->status = 0; break; }
         }
         if (P->restart && s->t % P->check_every == 0) {
             double S_a = score_of(s, s->xavg, s->yavg, &o);
@@ -680,6 +702,30 @@ void orc_corner_model(int32_t n, const double *x, const double *z, const double 
     }
     *fix_lb = fl;
     *fix_ub = fu;
+}
+
+/* Dual corner model (NEXT-4: "similar techniques ... to reduce the number of dual
+ * superbasic variables"; readings D-1..D-4).  From the phase-1
+ * point x, each column is classified against the original bounds with tolerance eps:
+ *   off   (x - l > eps and u - x > eps): lhat = -inf, uhat = +inf   -> its dual row
+ *         becomes the equality z_j = 0 (complementary slackness with x);
+ *   lower (x - l <= eps, l finite):       lhat = l,    uhat = +inf   -> z_j >= 0;
+ *   upper (otherwise, at a finite u):     lhat = -inf, uhat = u      -> z_j <= 0;
+ * so the model's dual feasible set is M's dual optimal face for x (D-1); A, b, c are
+ * unchanged (D-2).  Returns the three class counts in cnt[3]. */
+void orc_dual_corner_model(int32_t n, const double *x, const double *l, const double *u, double eps_abs,
+                           double *lhat, double *uhat, int64_t *cnt)
+{
+    cnt[0] = cnt[1] = cnt[2] = 0;
+    for (int32_t j = 0; j < n; ++j) {
+        if (x[j] - l[j] > eps_abs && u[j] - x[j] > eps_abs) {
+            lhat[j] = -INFINITY; uhat[j] = INFINITY; cnt[0]++;
+        } else if (x[j] - l[j] <= eps_abs && l[j] > -INFINITY) {
+            lhat[j] = l[j]; uhat[j] = INFINITY; cnt[1]++;
+        } else {
+            lhat[j] = -INFINITY; uhat[j] = u[j]; cnt[2]++;
+        }
+    }
 }
 
 /* Corner model row senses: an inequality row whose slack has a
