@@ -182,6 +182,25 @@ int cpd_corner_push(cpd_solver *s, const cpd_corner_params *cp, cpd_result *out,
  * off (restarts as configured) — lockstep parity with the oracle.  The first call
  * after create / cpd_set_iterate / cpd_solve starts a new run from the current
  * iterate (including the power iteration when step_size <= 0). */
+/* NEXT-4 dual corner push ("similar techniques ... to reduce the number of dual superbasic
+ * variables"; readings D-1..D-4).  From the solver's current (x, y)
+ * (normally the phase-1 solution): the dual corner model frees every column strictly off
+ * its bounds by > eps_abs (its dual row becomes z_j = 0), keeps [l, inf) for columns at a
+ * lower bound and (-inf, u] at an upper bound (so its dual feasible set is M's dual optimal
+ * face for x); PDHG (the solver's method) runs on it from (x, y), fresh primal weight,
+ * phase-1 step size, until k >= min_iters and every column's dual violation is <= eps_abs
+ * (or max_iters / time_limit).  The solver then holds (x, yhat): x is unchanged.  before /
+ * after (nullable): cpd_stats of (x, z) and (x, zhat); zero_rc (d) and est_dual_pushes
+ * (m - d) are the quantities the push lowers.  Uses eps_abs, min_iters, max_iters,
+ * time_limit_s, candidate_floor of `params` (NULL = defaults).  CPD_E_STATE for scaled or
+ * distributed problems. */
+int cpd_dual_corner_push(cpd_solver *s, const cpd_corner_params *params, cpd_result *out, cpd_stats *before,
+                         cpd_stats *after);
+/* On-the-fly choice of the push phases from phase-1 statistics (host only; reading D-4):
+ * primal = candidate criterion; dual = est_dual_pushes > 0 and
+ * min(m, off_bound) > zero_rc (the dual push can only bring the off-bound columns' reduced
+ * costs to 0). */
+int cpd_corner_decide(const cpd_stats *st, int32_t m, int32_t *primal, int32_t *dual);
 int cpd_step(cpd_solver *s, int64_t k);
 
 /* Current iterate: x[n], y[m], z[n] (z = c - A^T y for phase-1 y); any may be NULL. */

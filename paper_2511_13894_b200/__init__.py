@@ -33,7 +33,7 @@ DECLARED_SYMBOLS = [
     "cpd_get_kernel_times", "cpd_kernel_bytes", "cpd_solver_counters",
     "cpd_partition", "cpd_nccl_get_unique_id", "cpd_problem_create_dist", "cpd_problem_dist_info",
     "cpd_problem_scale", "cpd_problem_get_scaling", "cpd_problem_set_senses", "cpd_problem_plan_info",
-    "cpd_dist_layout",
+    "cpd_dist_layout", "cpd_dual_corner_push", "cpd_corner_decide",
 ]
 
 
@@ -106,6 +106,9 @@ def lib():
             "cpd_corner_push": (C.c_int, [P, C.POINTER(CornerParams), C.POINTER(Result),
                                           C.POINTER(Stats), C.POINTER(Stats)]),
             "cpd_step": (C.c_int, [P, I64]),
+            "cpd_dual_corner_push": (C.c_int, [P, C.POINTER(CornerParams), C.POINTER(Result), C.POINTER(Stats),
+                                               C.POINTER(Stats)]),
+            "cpd_corner_decide": (C.c_int, [C.POINTER(Stats), I32, C.POINTER(I32), C.POINTER(I32)]),
             "cpd_get_iterate": (C.c_int, [P, P, P, P, I32]),
             "cpd_set_iterate": (C.c_int, [P, P, P, I32]),
             "cpd_get_stats": (C.c_int, [P, I64, C.POINTER(Stats)]),
@@ -205,6 +208,16 @@ def dist_layout(m, n, ATp, ATj, world, partition, rank):
     keys = ("partition", "split", "L", "block_begin", "block_end", "own_len_m", "own_len_n", "gofs_m",
             "gofs_n", "poff_m", "poff_n", "local_rows_AT")
     return dict(zip(keys, out.tolist()))
+
+
+def corner_decide(st: dict, m: int):
+    """cpd_corner_decide (host only): (primal, dual) push phases from phase-1 statistics."""
+    S = Stats()
+    for k, _ in Stats._fields_:
+        setattr(S, k, int(st.get(k, 0)))
+    p, d = C.c_int32(), C.c_int32()
+    _check(lib().cpd_corner_decide(C.byref(S), int(m), C.byref(p), C.byref(d)))
+    return bool(p.value), bool(d.value)
 
 
 def nccl_unique_id() -> bytes:
@@ -393,6 +406,13 @@ class Solver:
         r, before, after = Result(), Stats(), Stats()
         _check(lib().cpd_corner_push(self.h, C.byref(cp), C.byref(r), C.byref(before), C.byref(after)))
         del keep
+        return as_dict(r), as_dict(before), as_dict(after)
+
+    def dual_corner_push(self, params: CornerParams = None, **kw):
+        """cpd_dual_corner_push (NEXT-4): (result, stats_before, stats_after)."""
+        cp = params or cpd_corner_params_default(**kw)
+        r, before, after = Result(), Stats(), Stats()
+        _check(lib().cpd_dual_corner_push(self.h, C.byref(cp), C.byref(r), C.byref(before), C.byref(after)))
         return as_dict(r), as_dict(before), as_dict(after)
 
     def step(self, k):

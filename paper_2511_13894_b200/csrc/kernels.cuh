@@ -73,7 +73,7 @@ constexpr int FIN_SPLIT = 1024;
 constexpr int TPB_F = 256;       // k_finish threads per CTA (1024 measured slower: 52 vs 45 us)
 constexpr int HOT_ROWS = 4096;   // y entries of the longest rows of A staged in k_sell's shared memory  // k_finish: rows with more partials get a CTA, the rest a warp
 
-enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2 };
+enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2, MODE_DUAL_ONLY = 3 };
 enum { ST_RUNNING = -1, ST_CONVERGED = 0, ST_ITER_LIMIT = 1, ST_TIME_LIMIT = 2, ST_FAIL = 3 };
 enum { GATE_ALWAYS = 0, GATE_K1 = 1, GATE_K2 = 2, GATE_CHECK = 3, GATE_RESTART = 4 };
 
@@ -316,8 +316,9 @@ __device__ __forceinline__ void score8(double rp2, double rd2, double pobj, doub
 // r_D_j = z - [l>-inf] max(z,0) + [u<inf] max(-z,0); bound part of the dual objective.
 // w: 1 / s_j of a diagonally scaled problem (z = z^ / s_j in the original space, the
 // violation scales the same way; the bound terms l^ z^+ = l z+ need no weight)
-__device__ __forceinline__ void dual_terms(double z, double lo, double hi, double& rd2, double& bnd,
-                                           double w = 1.0)
+// Returns r_D_j (the dual corner push counts |r_D_j| > eps_abs, reading D-3).
+__device__ __forceinline__ double dual_terms(double z, double lo, double hi, double& rd2, double& bnd,
+                                             double w = 1.0)
 {
     double zp = z > 0.0 ? z : 0.0;
     double zm = -z > 0.0 ? -z : 0.0;
@@ -326,6 +327,7 @@ __device__ __forceinline__ void dual_terms(double z, double lo, double hi, doubl
     if (hi < INFINITY) { rd += zm; bnd -= hi * zm; }
     rd *= w;
     rd2 += rd * rd;
+    return rd;
 }
 
 // Implicit inequality rows: sense 0 '=', 1 '<=' (Ax <= b),
@@ -1552,7 +1554,7 @@ struct PingPong {
 // bounds, PE = true: the corner model, or an LP with non-uniform bounds).
 template <bool PE>
 struct EpiPrimalT {
-    static constexpr int NS = 4;   // c^T x_k, ||r_D(y_k)||^2, bound terms, #nonfinite(x_{k+1})
+    static constexpr int NS = 5;   // c^T x_k, ||r_D(y_k)||^2, bound terms, #nonfinite(x_{k+1}), #{|r_D_j| > eps}
     static constexpr int NVEC = PE ? 5 : 3;
     static constexpr int PUSH = 1;
     __device__ __forceinline__ double pushval(int j) const { return xn[j]; }
@@ -1560,7 +1562,7 @@ struct EpiPrimalT {
     Bounds bd;
     PingPong X, Xa;
     // loaded
-    double tau, inv_t;
+    double tau, inv_t, eps_dual;
     const double* xc;
     double* xn;
     const double* xac;
@@ -1569,6 +1571,7 @@ struct EpiPrimalT {
     __device__ void load(const Ctl* ctl)
     {
         tau = ctl->tau;
+        eps_dual = ctl->eps_abs;
         inv_t = 1.0 / (double)(ctl->t + 1);
         xc = X.at(ctl->k);
         xn = X.at(ctl->k + 1);
@@ -1597,8 +1600,9 @@ struct EpiPrimalT {
         // averages are read once per iteration: streamed (evict-first) so L2 keeps x+
         __stcs(&xan[j], xa + (xp - xa) * inv_t);   // (x+ - x_avg)/t as a multiply (<= 1 ulp)
         acc[0] += cj * x;
-        dual_terms(z, lo, hi, acc[1], acc[2], w ? w[j] : 1.0);
+        const double rd = dual_terms(z, lo, hi, acc[1], acc[2], w ? w[j] : 1.0);
         acc[3] += isfinite(xp) ? 0.0 : 1.0;
+        acc[4] += fabs(rd) > eps_dual ? 1.0 : 0.0;
     }
     // F(k): termination of iterate k (k >= 1, not a check iteration), P:124-126 / P:391-395.
     __device__ void finalize(const double* tot, Ctl* ctl) const
@@ -1612,6 +1616,7 @@ struct EpiPrimalT {
         for (int i = 0; i < 8; ++i) ctl->last[i] = o[i];
         bool conv = false;
         if (ctl->mode == MODE_FULL) conv = o[7] <= ctl->eps_rel;
+        else if (ctl->mode == MODE_DUAL_ONLY) conv = k >= ctl->min_iters && tot[4] == 0.0;   // reading D-3
         else conv = k >= ctl->min_iters && o[0] <= ctl->target;
         if (conv) {
             ctl->done = 1; ctl->status = ST_CONVERGED; ctl->iterations = k;
@@ -1676,7 +1681,7 @@ struct EpiDual {
 
 // a7, A^T pass of a check: (A^T y_k), (A^T y_avg) -> current & average n-side terms.
 struct EpiCheckN {
-    static constexpr int NS = 9;   // ctx_c, rd2_c, bnd_c, dx2_c, ctx_a, rd2_a, bnd_a, dx2_a, off_bound(x_k; M)
+    static constexpr int NS = 10;  // ctx_c, rd2_c, bnd_c, dx2_c, ctx_a, rd2_a, bnd_a, dx2_a, off_bound(x_k; M), #{|r_D_j(y_k)| > eps}
     static constexpr int NVEC = 0;
     __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     const double* c;
@@ -1705,7 +1710,8 @@ struct EpiCheckN {
         const double xrj = xr[j];
         const double wj = w ? w[j] : 1.0;
         acc[0] += cj * x;
-        dual_terms(cj - s[0], lo, hi, acc[1], acc[2], wj);
+        const double rd = dual_terms(cj - s[0], lo, hi, acc[1], acc[2], wj);
+        acc[9] += fabs(rd) > eps_abs ? 1.0 : 0.0;
         acc[3] += (x - xrj) * (x - xrj);
         if (two) {
             const double xa = xac[j];
@@ -1765,6 +1771,10 @@ struct EpiCheckM {
             return;
         }
         if (ctl->mode == MODE_PRIMAL_ONLY && k >= ctl->min_iters && oc[0] <= ctl->target) {
+            ctl->done = 1; ctl->status = ST_CONVERGED; ctl->iterations = k;
+            return;
+        }
+        if (ctl->mode == MODE_DUAL_ONLY && k >= ctl->min_iters && en[9] == 0.0) {
             ctl->done = 1; ctl->status = ST_CONVERGED; ctl->iterations = k;
             return;
         }
@@ -1938,7 +1948,7 @@ struct EpiDualH {
 // Check of a Halpern run (every K): A^T yh -> score(zh), trajectory, restart
 // on the fixed-point residual, weight update from the anchor movement.
 struct EpiCheckH {
-    static constexpr int NS = 4;   // c^T xh, ||r_D(yh)||^2, bound terms, off-bound(xh; M)
+    static constexpr int NS = 5;   // c^T xh, ||r_D(yh)||^2, bound terms, off-bound(xh; M), #{|r_D_j(yh)| > eps}
     static constexpr int NVEC = 0;
     __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     const double* c;
@@ -1957,7 +1967,8 @@ struct EpiCheckH {
     {
         const double cj = c[j], x = xh[j];
         acc[0] += cj * x;
-        dual_terms(cj - s[0], bd.lo(j), bd.hi(j), acc[1], acc[2], w ? w[j] : 1.0);
+        const double rd = dual_terms(cj - s[0], bd.lo(j), bd.hi(j), acc[1], acc[2], w ? w[j] : 1.0);
+        acc[4] += fabs(rd) > eps_abs ? 1.0 : 0.0;
         if (traj) {
             const double xo = sx ? x * sx[j] : x;
             acc[3] += ((xo - orig.lo(j) > eps_abs) && (orig.hi(j) - xo > eps_abs)) ? 1.0 : 0.0;
@@ -1976,7 +1987,8 @@ struct EpiCheckH {
             ctl->traj_len += 1;
         }
         ctl->check_pending = 0;
-        if (ctl->mode == MODE_FULL && o[7] <= ctl->eps_rel) {
+        if ((ctl->mode == MODE_FULL && o[7] <= ctl->eps_rel) ||
+            (ctl->mode == MODE_DUAL_ONLY && k >= ctl->min_iters && tot[4] == 0.0)) {
             ctl->done = 1; ctl->status = ST_CONVERGED; ctl->iterations = k;
             return;
         }
@@ -2291,6 +2303,33 @@ struct OpSense {
         acc[0] += eq ? 1.0 : 0.0;
     }
     __device__ void finalize(const double* tot, Ctl* ctl) const { ctl->out[2] = tot[0]; }
+};
+
+// Dual corner model (NEXT-4, reading D-1): bounds that free the off-bound columns of the
+// phase-1 x (z_j = 0), keep z_j >= 0 at a lower bound and z_j <= 0 at an upper bound.
+struct OpDualModel {
+    static constexpr int NS = 3;   // off, lower, upper
+    const double* x;
+    Bounds bd;
+    double *lh, *uh;
+    double eps;
+    __device__ void load(const Ctl*) {}
+    __device__ __forceinline__ void elem(int64_t jj, double* acc) const
+    {
+        const int j = (int)jj;
+        const double xj = x[j], lo = bd.lo(j), hi = bd.hi(j);
+        if (xj - lo > eps && hi - xj > eps) {
+            lh[j] = -INFINITY; uh[j] = INFINITY; acc[0] += 1.0;
+        } else if (xj - lo <= eps && lo > -INFINITY) {
+            lh[j] = lo; uh[j] = INFINITY; acc[1] += 1.0;
+        } else {
+            lh[j] = -INFINITY; uh[j] = hi; acc[2] += 1.0;
+        }
+    }
+    __device__ void finalize(const double* tot, Ctl* ctl) const
+    {
+        for (int i = 0; i < NS; ++i) ctl->out[i] = tot[i];
+    }
 };
 
 // a10 corner statistics: counts as exact fp64 sums (< 2^53).

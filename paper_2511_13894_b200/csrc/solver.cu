@@ -578,13 +578,14 @@ using namespace cpd;
 
 enum { NODE_CHECK_N = 0, NODE_CHECK_M = 1, NODE_RESTART = 2, NODE_K0 = 3 };
 enum { KT_K1 = 0, KT_K2 = 1, KT_CN = 2, KT_CM = 3, KT_RS = 4, KT_N = 5 };
-static const char* KT_NAMES[2][KT_N] = {
+static const char* KT_NAMES[3][KT_N] = {
     {"primal_step_AT", "dual_step_A", "check_eval_AT", "check_eval_A", "restart_apply"},
     {"primal_step_AT:corner", "dual_step_A:corner", "check_eval_AT:corner", "check_eval_A:corner",
-     "restart_apply:corner"}};
+     "restart_apply:corner"},
+    {"primal_step_AT:dual", "dual_step_A:dual", "check_eval_AT:dual", "check_eval_A:dual", "restart_apply:dual"}};
 
 struct RunCfg {
-    int kind = 0;            // 0 original model, 1 corner model
+    int kind = 0;            // 0 original model, 1 corner model, 2 dual corner model (NEXT-4)
     int mode = MODE_FULL;
     int64_t max_iters = 0, min_iters = 0;
     double time_limit = 0.0;
@@ -604,6 +605,7 @@ struct cpd_solver {
     DBuf<double> X0, X1, Xa0, Xa1, Xr, Y, Ya, Yr, AX, AXa, Ystar, Z, lhat, uhat, chat, objd, SN, SM;
     DBuf<double> LHo, UHo, TX, TY, TY2;   // scaled problems: original-space model bounds; unscale scratch
     DBuf<double> XH, YH, AXH;         // Halpern: T(z) = (xh, yh) of the last iteration and A xh
+    DBuf<double> LHD, UHD, XS;        // dual corner model bounds; the phase-1 x it keeps
     DBuf<int8_t> shat;                // corner-model row senses
     DBuf<double> ACC;                 // short-row push sums (m), zero between iterations
     int64_t rows_eq = 0;
@@ -622,14 +624,14 @@ struct cpd_solver {
     bool eta_known = false;
     int64_t fix_lb = 0, fix_ub = 0;
     double corner_eps = 1e-6;
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
-    cudaGraph_t graph[2] = {nullptr, nullptr};
+    cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
+    cudaGraph_t graph[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> ev0, ev1;
-    double kt_ms[2][KT_N] = {};
-    int64_t kt_n[2][KT_N] = {};
+    double kt_ms[3][KT_N] = {};
+    int64_t kt_n[3][KT_N] = {};
     int nnodes = 0;
     const int64_t traj_cap = 1 << 16;
-    int64_t graph_kernels[2] = {0, 0};
+    int64_t graph_kernels[3] = {0, 0, 0};
     int64_t graph_launches = 0;
 
     cpd_solver(const cpd_problem* p, const cpd_params& pr) : P(p), prm(pr), cx(p)
@@ -673,7 +675,7 @@ struct cpd_solver {
     }
     ~cpd_solver()
     {
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < 3; ++k) {
             if (gexec[k]) cudaGraphExecDestroy(gexec[k]);
             if (graph[k]) cudaGraphDestroy(graph[k]);
         }
@@ -681,17 +683,22 @@ struct cpd_solver {
         for (auto e : ev1) cudaEventDestroy(e);
         if (h_active) cudaFreeHost(h_active);
     }
-    const int8_t* sense_of(int kind) const { return kind ? (P->has_sense ? shat.p : nullptr) : P->sense_own(); }
+    const int8_t* sense_of(int kind) const
+    {
+        return kind == 1 ? (P->has_sense ? shat.p : nullptr) : P->sense_own();
+    }
     const double* lh_orig() const { return P->scaled ? LHo.p : lhat.p; }
     const double* uh_orig() const { return P->scaled ? UHo.p : uhat.p; }
     int32_t nO() const { return P->own_len[1]; }
     int32_t mO() const { return P->own_len[0]; }
     double* Xp(int par) { return par ? X1.p : X0.p; }
 
-    const double* obj_of(int kind) const { return kind ? chat.p : P->c_own(); }
+    const double* obj_of(int kind) const { return kind == 1 ? chat.p : P->c_own(); }
     Bounds bounds_of(int kind) const
     {
-        return kind ? Bounds{lhat.p, uhat.p, 0.0, 0.0} : P->bounds_own();
+        if (kind == 1) return Bounds{lhat.p, uhat.p, 0.0, 0.0};
+        if (kind == 2) return Bounds{LHD.p, UHD.p, 0.0, 0.0};
+        return P->bounds_own();
     }
     // gather source of an owned vector of `side`: the replica when that side is split
     VecSel gsrc(int side, VecSel own, double* rep) const { return P->split == side ? fixed(rep) : own; }
@@ -874,11 +881,11 @@ struct cpd_solver {
             rec(ev0, n1);
             const VecSel ysrc = gsrc(0, fixed(Y.p), RV.p);
             if (kind == 0 && P->uniform_bounds) {   // scalar bounds: 3 staged per-row inputs
-                EpiPrimalT<false> e1{c, bd, X, Xa, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+                EpiPrimalT<false> e1{c, bd, X, Xa, 0.0, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr};
                 e1.w = P->w_n();
                 pass<1>(cx, 1, ysrc, none(), e1, g1);
             } else {
-                EpiPrimalT<true> e1{c, bd, X, Xa, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+                EpiPrimalT<true> e1{c, bd, X, Xa, 0.0, 0.0, 0.0, nullptr, nullptr, nullptr, nullptr};
                 e1.w = P->w_n();
                 pass<1>(cx, 1, ysrc, none(), e1, g1);
             }
@@ -1144,6 +1151,72 @@ struct cpd_solver {
             after->rows_eq = rows_eq;
         }
     }
+
+    // NEXT-4 dual corner push (readings D-1..D-3): PDHG on (A, b, c, lhat_D, uhat_D)
+    // from the current (x, y), stopped at k >= min_iters once every dual violation is
+    // <= eps_abs; returns (x, yhat, zhat) with x unchanged (phase 1's).
+    void dual_corner_push(const cpd_corner_params& cp, cpd_result* out, cpd_stats* before, cpd_stats* after)
+    {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (run_active) commit();
+        const int32_t n = nO(), m = mO();
+        corner_eps = cp.eps_abs;
+        if (!LHD.p) {
+            LHD.alloc(std::max(n, 1));
+            UHD.alloc(std::max(n, 1));
+            XS.alloc(std::max(n, 1));
+        }
+        const int g = std::min<int64_t>(cx.grid_elem, ((int64_t)std::max(n, m) + 255) / 256 + 1);
+        k_copy<<<g, 256, 0, cx.st>>>(n, XS.p, Xp(cur_par));   // the phase-1 x the push keeps
+        CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
+        if (before) {
+            compute_z();
+            eval_stats(cx, true, XS.p, Z.p, nullptr, nullptr, cp.eps_abs, cp.candidate_floor, 0, 0, before);
+        }
+        {   // D-1 bound map
+            AuxScope aux(cx);
+            Ctl h{};
+            h.K = 1;
+            cx.push_ctl(h);
+            OpDualModel od{XS.p, P->bounds_own(), LHD.p, UHD.p, cp.eps_abs};
+            elem(cx, n, od, always(), true);
+            cx.pull_ctl();
+            dual_counts[0] = (int64_t)cx.h_ctl->out[0];
+            dual_counts[1] = (int64_t)cx.h_ctl->out[1];
+            dual_counts[2] = (int64_t)cx.h_ctl->out[2];
+        }
+        if (!eta_known) {
+            if (prm.step_size > 0.0) eta_phase1 = prm.step_size;
+            else eta_phase1 = prm.step_scale / power_sigma(cx, prm.power_iters, prm.seed, 1.0, SN.p, SM.p);
+            eta_known = true;
+        }
+        RunCfg rc;
+        rc.kind = 2;
+        rc.mode = MODE_DUAL_ONLY;
+        rc.max_iters = cp.max_iters;
+        rc.min_iters = cp.min_iters;
+        rc.xs = XS.p;
+        rc.ys = Y.p;   // from (x*, y*)
+        rc.power = false;
+        rc.eta = eta_phase1;
+        rc.omega_in = 0.0;
+        begin(rc);
+        advance(cp.max_iters, cp.time_limit_s);
+        commit();
+        cx.sync();
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (out) fill_result(out, 2, wall);
+        k_copy<<<g, 256, 0, cx.st>>>(n, Xp(cur_par), XS.p);   // x stays phase 1's
+        CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
+        if (after) {
+            compute_z();
+            eval_stats(cx, true, XS.p, Z.p, nullptr, nullptr, cp.eps_abs, cp.candidate_floor, 0, 0, after);
+        }
+        run_active = false;
+    }
+    int64_t dual_counts[3] = {0, 0, 0};
 
     // x: n-side vector, y: m-side vector, both GLOBAL length; each rank takes its part.
     void set_iterate(const double* x, const double* y, int mem)
@@ -1575,6 +1648,30 @@ int cpd_corner_push(cpd_solver* s, const cpd_corner_params* cp, cpd_result* out,
     ABI_END
 }
 
+int cpd_dual_corner_push(cpd_solver* s, const cpd_corner_params* cp, cpd_result* out, cpd_stats* before,
+                         cpd_stats* after)
+{
+    ABI_BEGIN
+    if (!s) return fail(CPD_E_ARG, "NULL solver");
+    cpd_corner_params d;
+    cpd_corner_params_default(&d);
+    const cpd_corner_params& c = cp ? *cp : d;
+    if (!(c.eps_abs >= 0.0) || c.min_iters < 0 || c.max_iters < 0) return fail(CPD_E_ARG, "invalid corner parameter");
+    if (s->P->split >= 0 || s->P->scaled)
+        return fail(CPD_E_STATE, "the dual corner push needs an unscaled single-GPU problem");
+    CPD_CUDA(cudaSetDevice(s->P->device));
+    s->dual_corner_push(c, out, before, after);
+    ABI_END
+}
+
+int cpd_corner_decide(const cpd_stats* st, int32_t m, int32_t* primal, int32_t* dual)
+{
+    if (!st || !primal || !dual || m < 0) return fail(CPD_E_ARG, "NULL argument");
+    *primal = st->is_candidate ? 1 : 0;
+    *dual = (st->est_dual_pushes > 0 && std::min<int64_t>(m, st->off_bound) > st->zero_rc) ? 1 : 0;
+    return CPD_OK;
+}
+
 int cpd_step(cpd_solver* s, int64_t k)
 {
     ABI_BEGIN
@@ -1706,7 +1803,7 @@ int cpd_get_kernel_times(cpd_solver* s, const char** names, double* ms, int64_t*
     ABI_BEGIN
     if (!s || !len) return fail(CPD_E_ARG, "NULL argument");
     int32_t L = 0;
-    for (int kind = 0; kind < 2; ++kind)
+    for (int kind = 0; kind < 3; ++kind)
         for (int k = 0; k < KT_N; ++k) {
             if (L < cap) {
                 if (names) names[L] = KT_NAMES[kind][k];
