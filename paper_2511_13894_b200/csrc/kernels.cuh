@@ -1681,7 +1681,8 @@ struct EpiDual {
 
 // a7, A^T pass of a check: (A^T y_k), (A^T y_avg) -> current & average n-side terms.
 struct EpiCheckN {
-    static constexpr int NS = 10;  // ctx_c, rd2_c, bnd_c, dx2_c, ctx_a, rd2_a, bnd_a, dx2_a, off_bound(x_k; M), #{|r_D_j(y_k)| > eps}
+    static constexpr int NS = 11;  // ctx_c, rd2_c, bnd_c, dx2_c, ctx_a, rd2_a, bnd_a, dx2_a, off_bound(x_k; M),
+                                   // #{|r_D_j(y_k)| > eps}, off_bound(x_avg; M)
     static constexpr int NVEC = 0;
     __device__ __forceinline__ const double* vec(int) const { return nullptr; }
     const double* c;
@@ -1722,6 +1723,10 @@ struct EpiCheckN {
         if (traj) {
             const double xo = sx ? x * sx[j] : x;
             acc[8] += ((xo - orig.lo(j) > eps_abs) && (orig.hi(j) - xo > eps_abs)) ? 1.0 : 0.0;
+            if (two) {
+                const double xa = sx ? xac[j] * sx[j] : xac[j];
+                acc[10] += ((xa - orig.lo(j) > eps_abs) && (orig.hi(j) - xa > eps_abs)) ? 1.0 : 0.0;
+            }
         }
     }
     __device__ void finalize(const double* tot, Ctl* ctl) const
@@ -1752,6 +1757,17 @@ struct EpiCheckM {
         acc[2] += (yo - yri) * (yo - yri);
         acc[3] += (yav - yri) * (yav - yri);
     }
+    // Fig. 1 trajectory: the off-bound count and ||b - A x|| of the iterate
+    // the check leaves (the average when it restarts or returns there, else the current)
+    __device__ static void record(Ctl* ctl, int64_t k, double off, double rp)
+    {
+        if (ctl->traj_on && ctl->traj_len < ctl->traj_cap) {
+            ctl->traj_k[ctl->traj_len] = k;
+            ctl->traj_off[ctl->traj_len] = (int64_t)off;
+            ctl->traj_rp[ctl->traj_len] = rp;
+            ctl->traj_len += 1;
+        }
+    }
     __device__ void finalize(const double* tot, Ctl* ctl) const
     {
         const double* en = ctl->en;
@@ -1759,30 +1775,22 @@ struct EpiCheckM {
         double oc[8], oa[8];
         score8(ctl->rp2_cur, en[1], en[0], ctl->bty_cur + en[2], ctl->nb, ctl->nc, oc);
         for (int i = 0; i < 8; ++i) ctl->last[i] = oc[i];
-        if (ctl->traj_on && ctl->traj_len < ctl->traj_cap) {
-            ctl->traj_k[ctl->traj_len] = k;
-            ctl->traj_off[ctl->traj_len] = (int64_t)en[8];
-            ctl->traj_rp[ctl->traj_len] = oc[0];
-            ctl->traj_len += 1;
-        }
+        const double off_c = en[8], off_a = en[10], rp_a = sqrt(tot[0]);
         ctl->check_pending = 0;
-        if (ctl->mode == MODE_FULL && oc[7] <= ctl->eps_rel) {
+        if ((ctl->mode == MODE_FULL && oc[7] <= ctl->eps_rel) ||
+            (ctl->mode == MODE_PRIMAL_ONLY && k >= ctl->min_iters && oc[0] <= ctl->target) ||
+            (ctl->mode == MODE_DUAL_ONLY && k >= ctl->min_iters && en[9] == 0.0)) {
+            record(ctl, k, off_c, oc[0]);
             ctl->done = 1; ctl->status = ST_CONVERGED; ctl->iterations = k;
             return;
         }
-        if (ctl->mode == MODE_PRIMAL_ONLY && k >= ctl->min_iters && oc[0] <= ctl->target) {
-            ctl->done = 1; ctl->status = ST_CONVERGED; ctl->iterations = k;
-            return;
-        }
-        if (ctl->mode == MODE_DUAL_ONLY && k >= ctl->min_iters && en[9] == 0.0) {
-            ctl->done = 1; ctl->status = ST_CONVERGED; ctl->iterations = k;
-            return;
-        }
+        if (!ctl->restart_on) record(ctl, k, off_c, oc[0]);
         if (ctl->restart_on) {
             score8(tot[0], en[5], en[4], tot[1] + en[6], ctl->nb, ctl->nc, oa);
             const double S_c = oc[7], S_a = oa[7];
             if (ctl->mode == MODE_FULL && S_a <= ctl->eps_rel) {
                 for (int i = 0; i < 8; ++i) ctl->last[i] = oa[i];
+                record(ctl, k, off_a, rp_a);
                 ctl->done = 1; ctl->status = ST_CONVERGED; ctl->iterations = k;
                 ctl->returned_average = 1;
                 return;
@@ -1807,8 +1815,11 @@ struct EpiCheckM {
                 ctl->S_prev = INFINITY;
                 ctl->t = 0;
                 ctl->restarts += 1;
+                if (use_avg) record(ctl, k, off_a, rp_a);
+                else record(ctl, k, off_c, oc[0]);
             } else {
                 ctl->S_prev = S;
+                record(ctl, k, off_c, oc[0]);
             }
         }
         if (ctl->mode != MODE_NONE && k == ctl->max_iters) {
