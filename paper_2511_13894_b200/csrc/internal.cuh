@@ -216,6 +216,12 @@ namespace cpd {
 struct Ctx {
     const cpd_problem* P = nullptr;
     cudaStream_t st = nullptr;
+    // the dual step's heavy-row dense blocks run on `side`, concurrently with the other
+    // sub-kernels (DRAM-bound next to L2-bound), forked / joined with events on `st`
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool conc = true;
+    double dense_frac = 0.5;
     DBuf<Ctl> ctl_main, ctl_aux;      // run control block / scratch block for one-off evaluations
     Ctl* h_main = nullptr;           // pinned mirrors
     Ctl* h_aux = nullptr;

@@ -40,6 +40,11 @@ Ctx::Ctx(const cpd_problem* p) : P(p)
         if (g > 0) CPD_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)g));
     }
     CPD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CPD_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    CPD_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CPD_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    if (const char* e = getenv("CPD_CONC")) conc = e[0] != '0';
+    if (const char* e = getenv("CPD_DGRID")) dense_frac = std::min(1.0, std::max(0.05, atof(e)));
     ctl_main.alloc(1);
     ctl_aux.alloc(1);
     CPD_CUDA(cudaMemset(ctl_main.p, 0, sizeof(Ctl)));
@@ -80,6 +85,9 @@ Ctx::~Ctx()
     if (h_main) cudaFreeHost(h_main);
     if (h_aux) cudaFreeHost(h_aux);
     if (st) cudaStreamDestroy(st);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
 }
 
 DevPlan Ctx::planA() const
@@ -188,15 +196,26 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         const bool single = dp.nlong == 0;
         int prev = 0;
         Gate gs = g;
-        auto launch_dense = [&]() {
+        auto launch_dense = [&](bool concurrent = false) {
             if (dp.nheavy > 0) {   // heavy rows by dense column blocks (their slots, then k_finish)
                 const size_t DSM = (size_t)NV * HB * sizeof(double);
                 const int dgrid = occ_grid((const void*)k_dense<NV>, TPB_D, DSM, cx.P->num_sms);
-                const int grd = std::max(1, dgrid);   // item-balanced: every CTA busy
-                k_dense<NV><<<grd, TPB_D, DSM, cx.st>>>(M.dev(), dp, M.cols, v0, v1, g0, cx.ctl);
+                // item-balanced: every CTA busy; concurrent: a share of the machine
+                const int grd = std::max(1, concurrent ? (int)(dgrid * cx.dense_frac) : dgrid);
+                k_dense<NV><<<grd, TPB_D, DSM, concurrent ? cx.side : cx.st>>>(M.dev(), dp, M.cols, v0, v1, g0,
+                                                                               cx.ctl);
                 CPD_CUDA(cudaGetLastError());
                 ++cx.launches;
             }
+        };
+        const bool conc = cx.conc && dp.nheavy > 0;
+        auto fork = [&]() {
+            CPD_CUDA(cudaEventRecord(cx.ev_fork, cx.st));
+            CPD_CUDA(cudaStreamWaitEvent(cx.side, cx.ev_fork, 0));
+        };
+        auto join = [&]() {
+            CPD_CUDA(cudaEventRecord(cx.ev_join, cx.side));
+            CPD_CUDA(cudaStreamWaitEvent(cx.st, cx.ev_join, 0));
         };
         auto launch_items = [&](int a, int b, int fin, int slab = -1, int spass = 0) {
             DevPlan ds = dp;
@@ -226,6 +245,10 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
                 gs.active = nullptr;
                 return gr;
             };
+            if (conc) {   // heavy rows' dense blocks on the side stream, next to everything below
+                fork();
+                launch_dense(true);
+            }
             if (M.sell_half[0].on) {
                 static_assert(NV <= 2, "short_part holds two vectors");
                 sell_pass(M.dsell_half(0, cx.sshortA.p), M.sell_half[0].nslice, 0);   // no partials
@@ -233,8 +256,9 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
             } else {
                 prev += sell_pass(M.dsell_short(), M.sell_short.nslice, single ? 1 : 0);
             }
-            launch_dense();
+            if (!conc) launch_dense();
             if (!single && seg.back() > seg[1]) launch_items(seg[1], seg.back(), 0);
+            if (conc) join();
         } else if (M.plan.short_on && !(PushRole<Epi>::v == 2 && cx.push_acc)) {
             launch_dense();
             // the short rows' items once per column slab (each pass gathers from one
