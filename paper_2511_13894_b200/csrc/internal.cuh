@@ -71,6 +71,7 @@ struct Plan {
     std::vector<int32_t> seg;   // item ranges launched separately: rows items, then one per column slab
     int32_t nheavy = 0, nhb = 0;          // heavy rows (k_dense) and column blocks of HB
     DBuf<PlanEntry> dense_ent;            // {slot, block, q0, q1} grouped by block
+    DBuf<uint16_t> dense_col16;           // [nnz] column offset in the HB block of the heavy rows' entries
     DBuf<int32_t> dense_ptr;              // [nhb + 1] item range of each block
     int32_t dense_maxitems = 0;           // most items in one block (k_dense smem)
     // short rows by column slab (k_csrw slab mode): [nslab][rows + 1] pointers, entries slab-major

@@ -92,6 +92,7 @@ struct DevPlan {
     int32_t nheavy, nhb;       // heavy rows / dense column blocks (k_dense)
     const PlanEntry* dense_ent;   // {slot, block, q0, q1}: <= DCHUNK entries of one heavy row in one block
     const int32_t* dense_ptr;     // [nhb + 1] items of each block
+    const uint16_t* dense_col16;  // [nnz] heavy-row entries: column offset inside their HB block (12 -> 10 B/entry)
     int32_t dense_maxitems;       // most items in one block (k_dense item-sum smem)
     const int32_t* short_ptr;     // [nslab][rows + 1] short-row entries by slab (k_csrw slab mode)
     const int32_t* short_col;
@@ -268,6 +269,10 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p)
 #else
     return __ldcs(p);
 #endif
+}
+__device__ __forceinline__ int32_t ld_stream(const uint16_t* p)
+{
+    return (int32_t)__ldcs((const unsigned short*)p);
 }
 __device__ __forceinline__ double ld_stream(const double* p)
 {
@@ -1309,7 +1314,7 @@ k_csrw(DevCsr M, DevPlan P, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl
 // block of the vector once (coalesced) into shared memory, and every warp sums the
 // block's entries of its heavy rows from shared memory; one partial per (row,
 // block) goes to the row's slot for k_finish (fixed order: deterministic).
-template <int NV>
+template <int NV, bool C16 = false>   // C16: 16-bit in-block column offsets (P.dense_col16)
 __global__ void __launch_bounds__(TPB_D)
 k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ctl* ctl)
 {
@@ -1367,7 +1372,8 @@ k_dense(DevCsr M, DevPlan P, int32_t cols, VecSel vs0, VecSel vs1, Gate gate, Ct
 #pragma unroll
                 for (int u = 0; u < DU; ++u) {
                     const int qq = q + 32 * u;
-                    c[u] = qq < E.p1 ? ld_stream(M.j + qq) - j0 : -1;
+                    if constexpr (C16) c[u] = qq < E.p1 ? ld_stream(P.dense_col16 + qq) : -1;
+                    else c[u] = qq < E.p1 ? ld_stream(M.j + qq) - j0 : -1;
                     a[u] = qq < E.p1 ? ld_stream(M.x + qq) : 0.0;
                 }
 #pragma unroll

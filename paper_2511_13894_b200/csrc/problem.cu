@@ -60,6 +60,13 @@ __global__ void k_slab_pos(int32_t nl, int32_t nb, const int32_t* lrows, const i
     }
 }
 
+// col16[q] = col[q] mod HB for the entries q of heavy row rows[blockIdx.x]
+__global__ void k_col16(const int32_t* rows, const int32_t* p, const int32_t* col, uint16_t* col16)
+{
+    const int32_t r = rows[blockIdx.x];
+    for (int64_t q = p[r] + threadIdx.x; q < p[r + 1]; q += blockDim.x) col16[q] = (uint16_t)(col[q] & (HB - 1));
+}
+
 // Short rows (<= long_min entries) split by column slab: cnt[s * rows + r] = entries of
 // row r in slab s (0 for long rows); a row's columns are ascending, so the slab
 // boundaries are found by binary search.
@@ -277,6 +284,18 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
             maxit = std::max<int32_t>(maxit, (int32_t)dl[b].size());
         }
         plan.dense_maxitems = maxit;
+        // 16-bit column offsets of the heavy rows' entries (HB is a power of two <= 65536);
+        // CPD_DENSE16=0 keeps the 32-bit column indices
+        const char* d16 = getenv("CPD_DENSE16");
+        if (!(d16 && d16[0] == '0') && (HB & (HB - 1)) == 0 && HB <= 65536) {
+            plan.dense_col16.alloc((size_t)rp[rows]);
+            std::vector<int32_t> hr(nh);
+            for (int32_t h = 0; h < nh; ++h) hr[h] = lrows[heavy_l[h]];
+            DBuf<int32_t> dhr2(nh);
+            CPD_CUDA(cudaMemcpy(dhr2.p, hr.data(), sizeof(int32_t) * nh, cudaMemcpyHostToDevice));
+            k_col16<<<std::max(1, nh), 256>>>(dhr2.p, d_p, d_col, plan.dense_col16.p);
+            CPD_CUDA(cudaGetLastError());
+        }
         plan.dense_ent.alloc(std::max<size_t>(dent.size(), 1));
         plan.dense_ptr.alloc(nhb + 1);
         CPD_CUDA(cudaMemcpy(plan.dense_ent.p, dent.data(), sizeof(PlanEntry) * dent.size(), cudaMemcpyHostToDevice));

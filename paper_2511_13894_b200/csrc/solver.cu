@@ -94,7 +94,7 @@ DevPlan Ctx::planA() const
 {
     const Plan& pl = P->A.plan;
     return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
-                   pl.dense_ptr.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortA.p, nullptr,
+                   pl.dense_ptr.p, pl.dense_col16.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortA.p, nullptr,
                    pl.long_row.p,
                    pl.long_ptr.p, pl.long_ents.p, pl.nfin_heavy, lpartA.p};
 }
@@ -103,7 +103,7 @@ DevPlan Ctx::planAT() const
 {
     const Plan& pl = P->AT.plan;
     return DevPlan{pl.ent.p, pl.nent, pl.nlong, pl.warp ? 1 : GW, pl.nheavy, pl.nhb, pl.dense_ent.p,
-                   pl.dense_ptr.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortAT.p, nullptr,
+                   pl.dense_ptr.p, pl.dense_col16.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortAT.p, nullptr,
                    pl.long_row.p,
                    pl.long_ptr.p, pl.long_ents.p, pl.nfin_heavy, lpartAT.p};
 }
@@ -199,11 +199,14 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
         auto launch_dense = [&](bool concurrent = false) {
             if (dp.nheavy > 0) {   // heavy rows by dense column blocks (their slots, then k_finish)
                 const size_t DSM = (size_t)NV * HB * sizeof(double);
-                const int dgrid = occ_grid((const void*)k_dense<NV>, TPB_D, DSM, cx.P->num_sms);
+                const bool c16 = dp.dense_col16 != nullptr;
+                const void* kd = c16 ? (const void*)k_dense<NV, true> : (const void*)k_dense<NV, false>;
+                const int dgrid = occ_grid(kd, TPB_D, DSM, cx.P->num_sms);
                 // item-balanced: every CTA busy; concurrent: a share of the machine
                 const int grd = std::max(1, concurrent ? (int)(dgrid * cx.dense_frac) : dgrid);
-                k_dense<NV><<<grd, TPB_D, DSM, concurrent ? cx.side : cx.st>>>(M.dev(), dp, M.cols, v0, v1, g0,
-                                                                               cx.ctl);
+                cudaStream_t ss = concurrent ? cx.side : cx.st;
+                if (c16) k_dense<NV, true><<<grd, TPB_D, DSM, ss>>>(M.dev(), dp, M.cols, v0, v1, g0, cx.ctl);
+                else k_dense<NV, false><<<grd, TPB_D, DSM, ss>>>(M.dev(), dp, M.cols, v0, v1, g0, cx.ctl);
                 CPD_CUDA(cudaGetLastError());
                 ++cx.launches;
             }
