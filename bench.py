@@ -217,7 +217,8 @@ def reference_arm(args, lp, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args, lp, world),
+        "data": "synthetic", "config": {**workload_config(args, lp, world),
+                                         "parallelism": f"CPU oracle, single thread (rank 0 of {world})"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"{it} phase-1 iterations from x=0,y=0 per step on {lp.name} (full size)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -221,7 +221,7 @@ struct Ctx {
     // sub-kernels (DRAM-bound next to L2-bound), forked / joined with events on `st`
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    bool conc = true;
+    bool conc = false;   // CPD_CONC=1: measured neutral to -13% next to the 16-bit k_dense
     double dense_frac = 0.5;
     DBuf<Ctl> ctl_main, ctl_aux;      // run control block / scratch block for one-off evaluations
     Ctl* h_main = nullptr;           // pinned mirrors

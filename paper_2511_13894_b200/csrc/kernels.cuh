@@ -1552,7 +1552,8 @@ static __global__ void __launch_bounds__(TPB) k_copy_sel(int64_t N, double* dst,
 // Selects the ping-pong buffer of iterate k.
 struct PingPong {
     double* b[2];
-    __device__ __forceinline__ double* at(int64_t k) const { return b[k & 1]; }
+    // a select, not b[k & 1]: a dynamic index would put the epilogue struct in local memory
+    __device__ __forceinline__ double* at(int64_t k) const { return (k & 1) ? b[1] : b[0]; }
 };
 
 // a2 + a5 + n-side of a6, and the per-iteration termination decision F(k).
