@@ -112,3 +112,19 @@ def test_fullsize_termination(name):
         ref = oracle.stats(lp.m, xg, zg, lp.lb, lp.ub, model["lhat"], model["uhat"], 1e-6, 100_000)
         for k in ("off_bound", "off_bound_strict", "off_bound_model", "zero_rc", "candidates"):
             assert a[k] == ref[k], k
+
+
+def test_fullsize_c3_termination_halpern():
+    """Full C3 (4,000 x 4e6) to eps_rel = 1e-4 with the Halpern + PID method (NEXT-1),
+    where the oracle finishes in ~3 min (1,792 iterations; R-PDHG's 3,266 take ~7 min,
+    profiles/r02_oracle_tte.json): status, iterations +-1%, objective 1e-6."""
+    lp = lpgen.config("c3")
+    olp = oracle.OracleLP(lp)
+    P = cpd.Problem.from_lp(lp)
+    S = cpd.Solver(P, method=1, pid=1)
+    r = S.solve()
+    xo, yo, ro = oracle.solve(olp, oracle.default_params(method=1, pid=1))
+    assert r["status"] == ro["status"] == 0, (r, ro)
+    assert abs(r["iterations"] - ro["iterations"]) <= max(1, 0.01 * ro["iterations"]), (r, ro)
+    assert r["pobj"] == pytest.approx(ro["pobj"], rel=1e-6)
+    assert r["restarts"] == ro["restarts"]
