@@ -97,7 +97,8 @@ int cpd_problem_info(const cpd_problem *p, int64_t info[8]);
  * diagnostics: out[12] = {A warp plan (k_csrw) 1/0, A heavy rows (k_dense), A dense
  * column blocks, A column slabs of the long pieces, A short-row slab passes
  * (0 = off), A long rows, A long pieces, A rows items, A^T SELL-32 1/0, hot rows
- * (renumbered), A TMA plan entries (k_spmv), reserved 0}. */
+ * (renumbered), A TMA plan entries (k_spmv), columns renumbered 1/0}.  Renumbering is
+ * internal: every vector in or out of the ABI is in the caller's order. */
 int cpd_problem_plan_info(const cpd_problem *p, int64_t out[12]);
 
 /* Solver parameters (every constant of the R-PDHG reading, §8(c)). */

@@ -170,6 +170,9 @@ struct cpd_problem {
     cpd::DBuf<int32_t> rperm;
     std::vector<int32_t> h_rperm;
     int32_t hot = 0;
+    // ---- column renumbering: internal column k = user column cperm[k]
+    // (empty: the user's order); every n-vector crossing the ABI is mapped
+    cpd::DBuf<int32_t> cperm;
     // ---- short-row push: SELL(A^T) entries of short rows flagged
     bool push_on = false;
     int64_t push_nnz = 0;

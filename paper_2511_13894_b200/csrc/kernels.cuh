@@ -2217,10 +2217,11 @@ struct OpPowInit {
     uint64_t seed;
     int32_t n;
     int64_t jbase = 0;   // global index of local column 0 (distributed problems)
+    const int32_t* jmap = nullptr;   // user index of internal column j (column renumbering)
     __device__ void load(const Ctl*) {}
     __device__ __forceinline__ void elem(int64_t j, double* acc) const
     {
-        const double x = u01(seed, jbase + j) - 0.5;
+        const double x = u01(seed, jmap ? (int64_t)jmap[j] : jbase + j) - 0.5;
         v[j] = x;
         acc[0] += x * x;
     }
@@ -2272,6 +2273,7 @@ struct EpiCorner {
     double eps_abs, obj_scale;
     uint64_t seed;
     int64_t jbase = 0;   // global index of local column 0 (distributed problems)
+    const int32_t* jmap = nullptr;   // user index of internal column j (column renumbering)
     const double* w = nullptr;    // 1/s (scaled problem): the bound map tests z = z^ / s
     const double* sx = nullptr;   // s: objective of the corner model in the scaled space
     double* lho = nullptr;        // scaled problem: the model bounds in the original space
@@ -2290,7 +2292,7 @@ struct EpiCorner {
             lho[j] = zo < -eps_abs ? xj * sx[j] : ob.lo(j);
             uho[j] = zo > eps_abs ? xj * sx[j] : ob.hi(j);
         }
-        const double oj = obj ? obj[j] : obj_scale * u01(seed, jbase + j);
+        const double oj = obj ? obj[j] : obj_scale * u01(seed, jmap ? (int64_t)jmap[j] : jbase + j);
         chat[j] = sx ? oj * sx[j] : oj;
     }
     __device__ void finalize(const double* tot, Ctl* ctl) const

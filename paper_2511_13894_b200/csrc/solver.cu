@@ -527,6 +527,7 @@ static void power_iterate(Ctx& cx, Reps& rp, int32_t iters, uint64_t seed, doubl
 {
     const cpd_problem* P = cx.P;
     OpPowInit pi{v, seed, P->own_len[1], P->gofs[1]};
+    pi.jmap = P->cperm.p;   // U(seed, user column)
     elem(cx, P->own_len[1], pi, always(), true);
     for (int it = 0; it < iters; ++it) {
         EpiPowM pm{w, 0.0};
@@ -630,7 +631,7 @@ struct cpd_solver {
     Ctx cx;
     // state vectors: n-side (x-like) of length own_len[1], m-side (y-like) own_len[0]
     DBuf<double> X0, X1, Xa0, Xa1, Xr, Y, Ya, Yr, AX, AXa, Ystar, Z, lhat, uhat, chat, objd, SN, SM;
-    DBuf<double> LHo, UHo, TX, TY, TY2;   // scaled problems: original-space model bounds; unscale scratch
+    DBuf<double> LHo, UHo, TX, TY, TY2, TX2;   // scaled problems: original-space model bounds; unscale scratch
     DBuf<double> XH, YH, AXH;         // Halpern: T(z) = (xh, yh) of the last iteration and A xh
     DBuf<double> LHD, UHD, XS;        // dual corner model bounds; the phase-1 x it keeps
     DBuf<int8_t> shat;                // corner-model row senses
@@ -1105,6 +1106,11 @@ struct cpd_solver {
                                          cp.obj_mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice
                                                                   : cudaMemcpyHostToDevice,
                                          cx.st));
+            if (P->cperm.p) {   // user column order -> internal
+                ensure_tmp();
+                CPD_CUDA(cudaMemcpyAsync(TX.p, objd.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, cx.st));
+                perm_cols(objd.p, TX.p, 0);
+            }
             obj = objd.p;
         }
         // Algorithm 1 line 2: z*, bound map, objective
@@ -1116,6 +1122,7 @@ struct cpd_solver {
             cx.push_ctl(h);
             EpiCorner ec{P->c_own(), Xp(cur_par), P->bounds_own(), Z.p, lhat.p, uhat.p, chat.p, obj, cp.eps_abs,
                          cp.obj_scale, cp.seed, P->gofs[1]};
+            ec.jmap = P->cperm.p;   // Uniform objective by user column
             if (P->scaled) {   // bound map on z = z^/s; objective s * obj; model bounds also in the original space
                 if (!LHo.p) {
                     LHo.alloc(n);
@@ -1250,8 +1257,15 @@ struct cpd_solver {
     {
         const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         if (nO() > 0) {
-            if (x) CPD_CUDA(cudaMemcpyAsync(X0.p, x + P->gofs[1], sizeof(double) * nO(), kind, cx.st));
-            else CPD_CUDA(cudaMemsetAsync(X0.p, 0, sizeof(double) * nO(), cx.st));
+            if (x && P->cperm.p) {   // user column order -> internal
+                ensure_tmp();
+                CPD_CUDA(cudaMemcpyAsync(TX.p, x, sizeof(double) * nO(), kind, cx.st));
+                perm_cols(X0.p, TX.p, 0);
+            } else if (x) {
+                CPD_CUDA(cudaMemcpyAsync(X0.p, x + P->gofs[1], sizeof(double) * nO(), kind, cx.st));
+            } else {
+                CPD_CUDA(cudaMemsetAsync(X0.p, 0, sizeof(double) * nO(), cx.st));
+            }
         }
         if (mO() > 0) {
             if (y && P->hot) {   // user order -> internal row order
@@ -1282,6 +1296,7 @@ struct cpd_solver {
             TY.alloc(std::max(mO(), 1));
         }
         if (P->hot && !TY2.p) TY2.alloc(std::max(mO(), 1));
+        if (P->cperm.p && !TX2.p) TX2.alloc(std::max(nO(), 1));
     }
 
     void perm_vec(double* dst, const double* src, int mode)
@@ -1290,6 +1305,18 @@ struct cpd_solver {
         if (N <= 0) return;
         const int g = (int)std::min<int64_t>(cx.grid_elem, (N + 255) / 256);
         k_perm_vec<<<g, 256, 0, cx.st>>>(N, dst, src, P->rperm.p, mode);
+        CPD_CUDA(cudaGetLastError());
+        ++cx.launches;
+    }
+
+    // n-side vectors between the user's column order and the internal one (mode 0:
+    // user -> internal, 1: internal -> user); no-op copy when there is no renumbering
+    void perm_cols(double* dst, const double* src, int mode)
+    {
+        const int64_t N = nO();
+        if (N <= 0) return;
+        const int g = (int)std::min<int64_t>(cx.grid_elem, (N + 255) / 256);
+        k_perm_vec<<<g, 256, 0, cx.st>>>(N, dst, src, P->cperm.p, mode);
         CPD_CUDA(cudaGetLastError());
         ++cx.launches;
     }
@@ -1342,10 +1369,11 @@ struct cpd_solver {
     {
         if (z) compute_z();
         const double *xs = Xp(cur_par), *ys = Y.p, *zs = Z.p;
-        if (P->scaled || P->hot) {
+        if (P->scaled || P->hot || P->cperm.p) {
             ensure_tmp();
             if (x) {
                 if (P->scaled) scale_vec(nO(), TX.p, xs, P->ss.p, 1), xs = TX.p;
+                if (P->cperm.p) perm_cols(TX2.p, xs, 1), xs = TX2.p;   // internal -> user column order
                 gather_full(1, xs, x, mem);
             }
             if (y) {
@@ -1354,8 +1382,9 @@ struct cpd_solver {
                 gather_full(0, ys, y, mem);
             }
             if (z) {
-                cx.sync();   // TX reused
+                cx.sync();   // TX, TX2 reused
                 if (P->scaled) scale_vec(nO(), TX.p, zs, P->is.p, 1), zs = TX.p;
+                if (P->cperm.p) perm_cols(TX2.p, zs, 1), zs = TX2.p;
                 gather_full(1, zs, z, mem);
             }
             cx.sync();
@@ -1492,7 +1521,15 @@ int cpd_problem_get_scaling(const cpd_problem* p, double* r, double* s)
             for (int64_t k = 0; k < p->m; ++k) r[p->h_rperm[k]] = t[k];
         }
     }
-    if (s) CPD_CUDA(cudaMemcpy(s, p->ss.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
+    if (s) {
+        CPD_CUDA(cudaMemcpy(s, p->ss.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
+        if (p->cperm.p) {   // internal -> user column order
+            std::vector<int32_t> cp((size_t)p->n);
+            CPD_CUDA(cudaMemcpy(cp.data(), p->cperm.p, sizeof(int32_t) * p->n, cudaMemcpyDeviceToHost));
+            std::vector<double> t(s, s + p->n);
+            for (int64_t k = 0; k < p->n; ++k) s[cp[k]] = t[k];
+        }
+    }
     ABI_END
 }
 
@@ -1570,7 +1607,7 @@ int cpd_problem_plan_info(const cpd_problem* p, int64_t out[12])
     out[8] = p->AT.sell.on ? 1 : 0;
     out[9] = p->hot;
     out[10] = pl.warp ? 0 : pl.nent;
-    out[11] = 0;
+    out[11] = p->cperm.p ? 1 : 0;
     ABI_END
 }
 
@@ -1779,11 +1816,20 @@ int cpd_problem_score(const cpd_problem* p, const double* x, const double* y, in
     const int64_t nO = p->own_len[1], mO = p->own_len[0];
     DBuf<double> dx(std::max<int64_t>(nO, 1)), dy(std::max<int64_t>(mO, 1));
     const auto kind = mem == CPD_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (nO) CPD_CUDA(cudaMemcpy(dx.p, x + p->gofs[1], sizeof(double) * nO, kind));
-    if (mO) CPD_CUDA(cudaMemcpy(dy.p, y + p->gofs[0], sizeof(double) * mO, kind));
+    // every copy on the context's (non-blocking) stream, ordered with its kernels
+    if (nO) CPD_CUDA(cudaMemcpyAsync(dx.p, x + p->gofs[1], sizeof(double) * nO, kind, cx.st));
+    if (mO) CPD_CUDA(cudaMemcpyAsync(dy.p, y + p->gofs[0], sizeof(double) * mO, kind, cx.st));
+    cx.sync();
+    if (p->cperm.p && nO) {   // user column order -> internal
+        DBuf<double> t(nO);
+        CPD_CUDA(cudaMemcpyAsync(t.p, dx.p, sizeof(double) * nO, cudaMemcpyDeviceToDevice, cx.st));
+        k_perm_vec<<<(int)std::min<int64_t>(4096, (nO + 255) / 256), 256, 0, cx.st>>>(nO, dx.p, t.p, p->cperm.p, 0);
+        CPD_CUDA(cudaGetLastError());
+        cx.sync();
+    }
     if (p->hot && mO) {   // user row order -> internal
         DBuf<double> t(mO);
-        CPD_CUDA(cudaMemcpy(t.p, dy.p, sizeof(double) * mO, cudaMemcpyDeviceToDevice));
+        CPD_CUDA(cudaMemcpyAsync(t.p, dy.p, sizeof(double) * mO, cudaMemcpyDeviceToDevice, cx.st));
         k_perm_vec<<<(int)std::min<int64_t>(4096, (mO + 255) / 256), 256, 0, cx.st>>>(mO, dy.p, t.p, p->rperm.p, 0);
         CPD_CUDA(cudaGetLastError());
         cx.sync();
@@ -1817,9 +1863,18 @@ int cpd_compute_stats(const cpd_problem* p, const double* x, const double* z, co
     for (int i = 0; i < 4; ++i)
         if (src[i]) {
             b[i].alloc(std::max<int64_t>(nO, 1));
-            if (nO) CPD_CUDA(cudaMemcpy(b[i].p, src[i] + p->gofs[1], sizeof(double) * nO, kind));
+            if (nO) CPD_CUDA(cudaMemcpyAsync(b[i].p, src[i] + p->gofs[1], sizeof(double) * nO, kind, cx.st));
+            if (p->cperm.p && nO) {   // user column order -> internal
+                DBuf<double> t(nO);
+                CPD_CUDA(cudaMemcpyAsync(t.p, b[i].p, sizeof(double) * nO, cudaMemcpyDeviceToDevice, cx.st));
+                k_perm_vec<<<(int)std::min<int64_t>(4096, (nO + 255) / 256), 256, 0, cx.st>>>(nO, b[i].p, t.p,
+                                                                                            p->cperm.p, 0);
+                CPD_CUDA(cudaGetLastError());
+                cx.sync();
+            }
             dev[i] = b[i].p;
         }
+    cx.sync();
     eval_stats(cx, false, dev[0], dev[1], dev[2], dev[3], eps_abs, candidate_floor, 0, 0, out);
     ABI_END
 }
