@@ -648,6 +648,22 @@ static bool hot_rows_wanted(const cpd_problem* P, const std::vector<int32_t>& hp
 // single GPU, with the hot-row renumbering; CPD_COLSORT=0 disables.
 static void transpose(int32_t rows, int32_t cols, int64_t nnz, const int32_t* p, const int32_t* j,
                       const double* x, int32_t* tp, int32_t* tj, double* tx, int sms);
+// new row k = old row perm[k] for a layout of short rows: a warp per row, lane-strided
+// copy (coalesced; k_permute_rows' per-entry search is for rows of any length)
+__global__ void k_permute_rows_warp(int32_t rows, const int32_t* perm, const int32_t* op, const int32_t* oj,
+                                    const double* ox, const int32_t* np, int32_t* nj, double* nx)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < rows;
+         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t src = op[perm[k]], len = op[perm[k] + 1] - src, dst = np[k];
+        for (int32_t q = lane; q < len; q += 32) {
+            nj[dst + q] = oj[src + q];
+            nx[dst + q] = ox[src + q];
+        }
+    }
+}
+
 __global__ void k_rank_rows(int32_t rows, const int32_t* perm, int32_t* rank)
 {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < rows; k += (int64_t)gridDim.x * blockDim.x)
@@ -709,7 +725,8 @@ static void renumber_cols(cpd_problem* P, const std::vector<int32_t>& hp)
     CPD_CUDA(cub::DeviceScan::ExclusiveSum(stmp.p, sb, nlen.p, ntp.p, n + 1));
     DBuf<int32_t> nj(std::max<int64_t>(nnz, 1));
     DBuf<double> nx(std::max<int64_t>(nnz, 1));
-    k_permute_rows<<<grid(nnz), 256>>>(n, nnz, cperm.p, P->AT.p.p, P->AT.j.p, P->AT.x.p, ntp.p, nj.p, nx.p);
+    k_permute_rows_warp<<<(int)std::min<int64_t>(((int64_t)n * 32 + 255) / 256, (int64_t)sms * 64), 256>>>(
+        n, cperm.p, P->AT.p.p, P->AT.j.p, P->AT.x.p, ntp.p, nj.p, nx.p);
     CPD_CUDA(cudaGetLastError());
     P->AT.p = std::move(ntp);
     P->AT.j = std::move(nj);
