@@ -61,10 +61,14 @@ __global__ void k_slab_pos(int32_t nl, int32_t nb, const int32_t* lrows, const i
 }
 
 // col16[q] = col[q] mod HB for the entries q of heavy row rows[blockIdx.x]
+// (grid: blockIdx.y = heavy row, blockIdx.x strides its entries: the Zipf head's rows
+// hold millions of entries each)
 __global__ void k_col16(const int32_t* rows, const int32_t* p, const int32_t* col, uint16_t* col16)
 {
-    const int32_t r = rows[blockIdx.x];
-    for (int64_t q = p[r] + threadIdx.x; q < p[r + 1]; q += blockDim.x) col16[q] = (uint16_t)(col[q] & (HB - 1));
+    const int32_t r = rows[blockIdx.y];
+    for (int64_t q = p[r] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p[r + 1];
+         q += (int64_t)gridDim.x * blockDim.x)
+        col16[q] = (uint16_t)(col[q] & (HB - 1));
 }
 
 // Short rows (<= long_min entries) split by column slab: cnt[s * rows + r] = entries of
@@ -293,7 +297,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
             for (int32_t h = 0; h < nh; ++h) hr[h] = lrows[heavy_l[h]];
             DBuf<int32_t> dhr2(nh);
             CPD_CUDA(cudaMemcpy(dhr2.p, hr.data(), sizeof(int32_t) * nh, cudaMemcpyHostToDevice));
-            k_col16<<<std::max(1, nh), 256>>>(dhr2.p, d_p, d_col, plan.dense_col16.p);
+            k_col16<<<dim3(64, std::max(1, nh)), 256>>>(dhr2.p, d_p, d_col, plan.dense_col16.p);
             CPD_CUDA(cudaGetLastError());
         }
         plan.dense_ent.alloc(std::max<size_t>(dent.size(), 1));
