@@ -560,22 +560,6 @@ void build_short_sell(Matrix& M, const std::vector<int32_t>& rp)
 }
 
 // ------------------------------------------------------------ hot-row renumbering
-// new row k of A = old row perm[k]: entry-parallel copy (a warp per row would leave
-// C5's 1.8e7-entry top row to one warp); the row of new position d by binary search
-__global__ void k_permute_rows(int32_t rows, int64_t nnz, const int32_t* perm, const int32_t* op,
-                               const int32_t* oj, const double* ox, const int32_t* np, int32_t* nj, double* nx)
-{
-    for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < nnz; d += (int64_t)gridDim.x * blockDim.x) {
-        int32_t lo = 0, hi = rows;   // np[lo] <= d < np[hi]
-        while (hi - lo > 1) {
-            const int32_t mid = lo + (hi - lo) / 2;
-            if (np[mid] <= d) lo = mid; else hi = mid;
-        }
-        const int64_t src = op[perm[lo]] + (d - np[lo]);
-        nj[d] = oj[src];
-        nx[d] = ox[src];
-    }
-}
 __global__ void k_remap(int64_t N, int32_t* j, const int32_t* pinv)
 {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x)
@@ -593,27 +577,6 @@ thread_local bool g_no_renumber = false;
 // hold >= 30% of the nonzeros (C5's Zipf rows): the most-gathered entries of y then
 // form a prefix that k_sell keeps in shared memory.  Every y-side
 // array is stored in this internal order; the ABI maps y / b / senses / r.
-// ascending key = descending length; ties among short rows (<= WLONG entries) broken by
-// decreasing count of entries in the first column half [0, half), so a SELL slice of
-// 32 consecutive short rows is also even in each half (short-row SELL passes, §6)
-__global__ void k_len_keys(int32_t rows, const int32_t* p, const int32_t* col, int32_t half, int32_t maxlen,
-                           uint64_t* key, int32_t* val)
-{
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t a = p[r], b = p[r + 1], len = b - a;
-        uint64_t sec = 0;
-        if (len <= WLONG) {
-            int32_t lo = a, hi = b;   // first entry with col >= half
-            while (lo < hi) {
-                const int32_t mid = lo + (hi - lo) / 2;
-                if (col[mid] < half) lo = mid + 1; else hi = mid;
-            }
-            sec = (uint64_t)(WLONG - (lo - a));
-        }
-        key[r] = ((uint64_t)(maxlen - len) << 8) | sec;
-        val[r] = (int32_t)r;
-    }
-}
 __global__ void k_perm_lens(int32_t rows, const int32_t* perm, const int32_t* p, int32_t* len, int32_t* pinv)
 {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < rows; k += (int64_t)gridDim.x * blockDim.x) {
@@ -653,7 +616,7 @@ static bool hot_rows_wanted(const cpd_problem* P, const std::vector<int32_t>& hp
 static void transpose(int32_t rows, int32_t cols, int64_t nnz, const int32_t* p, const int32_t* j,
                       const double* x, int32_t* tp, int32_t* tj, double* tx, int sms);
 // new row k = old row perm[k] for a layout of short rows: a warp per row, lane-strided
-// copy (coalesced; k_permute_rows' per-entry search is for rows of any length)
+// copy (coalesced; the rows of CSR(A^T) are short)
 __global__ void k_permute_rows_warp(int32_t rows, const int32_t* perm, const int32_t* op, const int32_t* oj,
                                     const double* ox, const int32_t* np, int32_t* nj, double* nx)
 {
@@ -665,6 +628,31 @@ __global__ void k_permute_rows_warp(int32_t rows, const int32_t* perm, const int
             nj[dst + q] = oj[src + q];
             nx[dst + q] = ox[src + q];
         }
+    }
+}
+
+// short rows' entry count in the first half of the NEW column order (tie-break of the
+// row renumbering, so a SELL slice of short rows is even in both column halves)
+__global__ void k_h0_count(int32_t n, const int32_t* tp, const int32_t* tj, const int32_t* cpinv, const int32_t* ap,
+                           int32_t half, int32_t* h0)
+{
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t nj = cpinv ? cpinv[j] : (int32_t)j;
+        if (nj >= half) continue;
+        for (int32_t q = tp[j]; q < tp[j + 1]; ++q) {
+            const int32_t i = tj[q];
+            if (ap[i + 1] - ap[i] <= WLONG) atomicAdd(&h0[i], 1);
+        }
+    }
+}
+__global__ void k_len_keys_h0(int32_t rows, const int32_t* p, const int32_t* h0, int32_t maxlen, uint64_t* key,
+                              int32_t* val)
+{
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t len = p[r + 1] - p[r];
+        const uint64_t sec = len <= WLONG ? (uint64_t)(WLONG - h0[r]) : 0;
+        key[r] = ((uint64_t)(maxlen - len) << 8) | sec;
+        val[r] = (int32_t)r;
     }
 }
 
@@ -686,110 +674,101 @@ __global__ void k_col_keys(int32_t n, const int32_t* tp, const int32_t* tj, cons
         val[j] = (int32_t)j;
     }
 }
-static void renumber_cols(cpd_problem* P, const std::vector<int32_t>& hp)
+// Combined renumbering from CSR(A^T), one transpose:
+//  rows of A by decreasing length (hot-row renumbering; short rows tie-broken by their
+//  entry count in the first half of the NEW column order), and, unless CPD_COLSORT=0,
+//  columns by the length rank of their longest non-heavy row (column renumbering).
+//  CSR(A^T) gets its rows permuted (columns) and its entries remapped (rows); CSR(A) is
+//  then the stable transpose of it, so every row of A has ascending (new) columns.
+static void renumber(cpd_problem* P, std::vector<int32_t>& hp)
 {
-    const char* e = getenv("CPD_COLSORT");
-    if (e && e[0] == '0') return;
     int32_t maxlen = 0;
     if (!hot_rows_wanted(P, hp, &maxlen)) return;
+    const char* e = getenv("CPD_COLSORT");
+    const bool cols_on = !(e && e[0] == '0');
     const int32_t m = P->m, n = P->n;
     const int64_t nnz = P->nnz;
     const int sms = P->num_sms;
     auto grid = [&](int64_t N) { return (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, (int64_t)sms * 16)); };
-    // rank of every row by (length desc, index)
-    DBuf<int32_t> lkey(m), lkey2(m), lval(m), rperm(m), rank(m);
-    {
-        DBuf<uint64_t> k64(m), k64b(m);
-        k_len_keys<<<grid(m), 256>>>(m, P->A.p.p, P->A.j.p, 0, maxlen, k64.p, lval.p);   // (no tie-break: half 0)
-        int end_bit = 9;
-        while ((1LL << (end_bit - 8)) <= (long long)maxlen) ++end_bit;
-        size_t tb = 0;
-        CPD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k64.p, k64b.p, lval.p, rperm.p, m, 0, end_bit));
-        DBuf<unsigned char> tmp(tb);
-        CPD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k64.p, k64b.p, lval.p, rperm.p, m, 0, end_bit));
-    }
-    k_rank_rows<<<grid(m), 256>>>(m, rperm.p, rank.p);
-    // column keys and the stable sort
-    DBuf<int32_t> ckey(n), ckey2(n), cval(n), cperm(n), cpinv(n), nlen((size_t)n + 1), ntp((size_t)n + 1);
-    k_col_keys<<<grid(n), 256>>>(n, P->AT.p.p, P->AT.j.p, rank.p, P->A.p.p, heavy_min(), m, ckey.p, cval.p);
-    {
-        int end_bit = 1;
-        while ((1LL << end_bit) <= (long long)m) ++end_bit;
-        size_t tb = 0;
-        CPD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ckey.p, ckey2.p, cval.p, cperm.p, n, 0, end_bit));
-        DBuf<unsigned char> tmp(tb);
-        CPD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, ckey.p, ckey2.p, cval.p, cperm.p, n, 0, end_bit));
-    }
-    // CSR(A^T) rows in the new column order
-    k_perm_lens<<<grid(n), 256>>>(n, cperm.p, P->AT.p.p, nlen.p, cpinv.p);
-    CPD_CUDA(cudaMemset(nlen.p + n, 0, sizeof(int32_t)));
-    size_t sb = 0;
-    CPD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, nlen.p, ntp.p, n + 1));
-    DBuf<unsigned char> stmp(sb);
-    CPD_CUDA(cub::DeviceScan::ExclusiveSum(stmp.p, sb, nlen.p, ntp.p, n + 1));
-    DBuf<int32_t> nj(std::max<int64_t>(nnz, 1));
-    DBuf<double> nx(std::max<int64_t>(nnz, 1));
-    k_permute_rows_warp<<<(int)std::min<int64_t>(((int64_t)n * 32 + 255) / 256, (int64_t)sms * 64), 256>>>(
-        n, cperm.p, P->AT.p.p, P->AT.j.p, P->AT.x.p, ntp.p, nj.p, nx.p);
-    CPD_CUDA(cudaGetLastError());
-    P->AT.p = std::move(ntp);
-    P->AT.j = std::move(nj);
-    P->AT.x = std::move(nx);
-    // CSR(A) with the new column indices, each row sorted: the transpose of the new CSR(A^T)
-    transpose(n, m, nnz, P->AT.p.p, P->AT.j.p, P->AT.x.p, P->A.p.p, P->A.j.p, P->A.x.p, sms);
-    // c and (non-uniform) bounds in the new order
-    DBuf<double> t(std::max(n, 1));
-    auto gather = [&](DBuf<double>& v) {
-        k_gather_d<<<grid(n), 256>>>(n, t.p, v.p, cperm.p);
-        CPD_CUDA(cudaMemcpy(v.p, t.p, sizeof(double) * n, cudaMemcpyDeviceToDevice));
-    };
-    gather(P->c);
-    if (!P->uniform_bounds) {
-        gather(P->lb);
-        gather(P->ub);
-    }
-    CPD_CUDA(cudaGetLastError());
-    CPD_CUDA(cudaDeviceSynchronize());
-    P->cperm = std::move(cperm);
-}
-
-static void renumber_rows(cpd_problem* P, std::vector<int32_t>& hp)
-{
-    const int32_t m = P->m;
-    int32_t maxlen = 0;
-    if (!hot_rows_wanted(P, hp, &maxlen)) return;
-    const int sms = P->num_sms;
-    auto grid = [&](int64_t N) { return (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, (int64_t)sms * 16)); };
-    // stable device sort by decreasing length (radix sort is stable)
-    DBuf<uint64_t> key(m), key2(m);
-    DBuf<int32_t> val(m), dperm(m), dpinv(m), nlen((size_t)m + 1), dnp((size_t)m + 1);
-    k_len_keys<<<grid(m), 256>>>(m, P->A.p.p, P->A.j.p, (int32_t)((P->n + 1) / 2), maxlen, key.p, val.p);
     int end_bit = 9;
     while ((1LL << (end_bit - 8)) <= (long long)maxlen) ++end_bit;
-    size_t tb = 0;
-    CPD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, val.p, dperm.p, m, 0, end_bit));
-    DBuf<unsigned char> tmp(tb);
-    CPD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key2.p, val.p, dperm.p, m, 0, end_bit));
-    k_perm_lens<<<grid(m), 256>>>(m, dperm.p, P->A.p.p, nlen.p, dpinv.p);
-    CPD_CUDA(cudaMemset(nlen.p + m, 0, sizeof(int32_t)));
-    size_t sb = 0;
-    CPD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, nlen.p, dnp.p, m + 1));
-    DBuf<unsigned char> stmp(sb);
-    CPD_CUDA(cub::DeviceScan::ExclusiveSum(stmp.p, sb, nlen.p, dnp.p, m + 1));
-    DBuf<int32_t> nj(std::max<int64_t>(P->nnz, 1));
-    DBuf<double> nx(std::max<int64_t>(P->nnz, 1)), nb(m);
-    k_permute_rows<<<grid(P->nnz), 256>>>(m, P->nnz, dperm.p, P->A.p.p, P->A.j.p, P->A.x.p, dnp.p, nj.p, nx.p);
-    k_remap<<<grid(P->nnz), 256>>>(P->nnz, P->AT.j.p, dpinv.p);
-    k_gather_d<<<grid(m), 256>>>(m, nb.p, P->b.p, dperm.p);
+    auto sort_rows = [&](const DBuf<uint64_t>& k, DBuf<int32_t>& val, DBuf<int32_t>& perm) {
+        DBuf<uint64_t> k2(m);
+        size_t tb = 0;
+        CPD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k.p, k2.p, val.p, perm.p, m, 0, end_bit));
+        DBuf<unsigned char> tmp(tb);
+        CPD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k.p, k2.p, val.p, perm.p, m, 0, end_bit));
+    };
+    DBuf<uint64_t> key(m);
+    DBuf<int32_t> val(m), h0(m), rperm(m), rpinv(m);
+    CPD_CUDA(cudaMemset(h0.p, 0, sizeof(int32_t) * m));
+    DBuf<int32_t> cperm, cpinv;
+    if (cols_on) {
+        // rank of every row by length (ties: index), the column keys, their stable sort
+        DBuf<int32_t> rank(m), rp0(m);
+        k_len_keys_h0<<<grid(m), 256>>>(m, P->A.p.p, h0.p, maxlen, key.p, val.p);   // h0 = 0: length only
+        sort_rows(key, val, rp0);
+        k_rank_rows<<<grid(m), 256>>>(m, rp0.p, rank.p);
+        DBuf<int32_t> ckey(n), ckey2(n), cval(n);
+        cperm.alloc(n);
+        cpinv.alloc(n);
+        k_col_keys<<<grid(n), 256>>>(n, P->AT.p.p, P->AT.j.p, rank.p, P->A.p.p, heavy_min(), m, ckey.p, cval.p);
+        int cb = 1;
+        while ((1LL << cb) <= (long long)m) ++cb;
+        size_t tb = 0;
+        CPD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ckey.p, ckey2.p, cval.p, cperm.p, n, 0, cb));
+        DBuf<unsigned char> tmp(tb);
+        CPD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, ckey.p, ckey2.p, cval.p, cperm.p, n, 0, cb));
+        k_rank_rows<<<grid(n), 256>>>(n, cperm.p, cpinv.p);   // cpinv[old column] = new column
+    }
+    // rows: length, then first-half count in the new column order
+    k_h0_count<<<grid(n), 256>>>(n, P->AT.p.p, P->AT.j.p, cols_on ? cpinv.p : nullptr, P->A.p.p,
+                                 (int32_t)((n + 1) / 2), h0.p);
+    k_len_keys_h0<<<grid(m), 256>>>(m, P->A.p.p, h0.p, maxlen, key.p, val.p);
+    sort_rows(key, val, rperm);
+    k_rank_rows<<<grid(m), 256>>>(m, rperm.p, rpinv.p);   // rpinv[old row] = new row
+    // CSR(A^T): rows in the new column order, entries renamed to the new rows
+    if (cols_on) {
+        DBuf<int32_t> nlen((size_t)n + 1), ntp((size_t)n + 1), tmpinv(n);
+        k_perm_lens<<<grid(n), 256>>>(n, cperm.p, P->AT.p.p, nlen.p, tmpinv.p);
+        CPD_CUDA(cudaMemset(nlen.p + n, 0, sizeof(int32_t)));
+        size_t sb = 0;
+        CPD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, nlen.p, ntp.p, n + 1));
+        DBuf<unsigned char> stmp(sb);
+        CPD_CUDA(cub::DeviceScan::ExclusiveSum(stmp.p, sb, nlen.p, ntp.p, n + 1));
+        DBuf<int32_t> nj(std::max<int64_t>(nnz, 1));
+        DBuf<double> nx(std::max<int64_t>(nnz, 1));
+        k_permute_rows_warp<<<(int)std::min<int64_t>(((int64_t)n * 32 + 255) / 256, (int64_t)sms * 64), 256>>>(
+            n, cperm.p, P->AT.p.p, P->AT.j.p, P->AT.x.p, ntp.p, nj.p, nx.p);
+        CPD_CUDA(cudaGetLastError());
+        P->AT.p = std::move(ntp);
+        P->AT.j = std::move(nj);
+        P->AT.x = std::move(nx);
+    }
+    k_remap<<<grid(nnz), 256>>>(nnz, P->AT.j.p, rpinv.p);
+    // CSR(A) = the stable transpose: new rows, ascending new columns
+    transpose(n, m, nnz, P->AT.p.p, P->AT.j.p, P->AT.x.p, P->A.p.p, P->A.j.p, P->A.x.p, sms);
+    // vectors in the new orders
+    DBuf<double> t(std::max(std::max(n, m), 1));
+    k_gather_d<<<grid(m), 256>>>(m, t.p, P->b.p, rperm.p);
+    CPD_CUDA(cudaMemcpy(P->b.p, t.p, sizeof(double) * m, cudaMemcpyDeviceToDevice));
+    if (cols_on) {
+        auto gather = [&](DBuf<double>& v) {
+            k_gather_d<<<grid(n), 256>>>(n, t.p, v.p, cperm.p);
+            CPD_CUDA(cudaMemcpy(v.p, t.p, sizeof(double) * n, cudaMemcpyDeviceToDevice));
+        };
+        gather(P->c);
+        if (!P->uniform_bounds) {
+            gather(P->lb);
+            gather(P->ub);
+        }
+    }
     CPD_CUDA(cudaGetLastError());
     P->h_rperm.resize(m);
-    CPD_CUDA(cudaMemcpy(P->h_rperm.data(), dperm.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
-    CPD_CUDA(cudaMemcpy(hp.data(), dnp.p, sizeof(int32_t) * ((size_t)m + 1), cudaMemcpyDeviceToHost));
-    CPD_CUDA(cudaMemcpy(P->b.p, nb.p, sizeof(double) * m, cudaMemcpyDeviceToDevice));
-    P->A.p = std::move(dnp);
-    P->A.j = std::move(nj);
-    P->A.x = std::move(nx);
-    P->rperm = std::move(dperm);
+    CPD_CUDA(cudaMemcpy(P->h_rperm.data(), rperm.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+    CPD_CUDA(cudaMemcpy(hp.data(), P->A.p.p, sizeof(int32_t) * ((size_t)m + 1), cudaMemcpyDeviceToHost));
+    P->rperm = std::move(rperm);
+    if (cols_on) P->cperm = std::move(cperm);
     P->hot = HOT_ROWS;
 }
 
@@ -1231,10 +1210,8 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         std::vector<int32_t> hp((size_t)m + 1), htp((size_t)n + 1);
         CPD_CUDA(cudaMemcpy(hp.data(), P->A.p.p, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost));
         tm.mark("rowptr D2H");
-        renumber_cols(P, hp);
-        tm.mark("renumber columns");
-        renumber_rows(P, hp);
-        tm.mark("renumber");
+        renumber(P, hp);
+        tm.mark("renumber rows + columns");
         // A: warp-item plan for k_csrw unless CPD_WARP=0 (then the TMA plan of k_spmv)
         // default: warp plan when rows longer than WLONG carry >= 25% of the nonzeros
         // (C3, C5: measured faster); short-row matrices keep the TMA plan (C2, C4)
