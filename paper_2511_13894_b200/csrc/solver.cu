@@ -1400,7 +1400,7 @@ struct cpd_solver {
     {
         // local (this rank's) algorithmic bytes: matrix block + owned vectors + gathered vector
         const double nnz = (double)P->nnz, nr = P->n, mr = P->m, n = nO(), m = mO();
-        const bool corner = name.find(":corner") != std::string::npos;
+        const bool corner = name.find(":corner") != std::string::npos || name.find(":dual") != std::string::npos;
         const std::string base = name.substr(0, name.find(':'));
         const double bnd = (corner || !P->uniform_bounds) ? 16.0 * n : 0.0;
         // short-row push: their entries are read again by K1 (12 B) and not by K2; K2
