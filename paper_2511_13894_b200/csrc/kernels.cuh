@@ -949,6 +949,17 @@ struct DevSell {
 };
 
 constexpr int TPB_SELL = 256;
+// SELL entry layout inside a slice: SELL_PAIR = 1 stores entries k, k+1 of a lane next to
+// each other ([k / 2][lane][k % 2], slice width even), so a lane streams them with one
+// 8-byte (index) and one 16-byte (value) load: coalesced AND vectorised; 0 = [k][lane].
+#ifndef CPD_SELL_PAIR
+#define CPD_SELL_PAIR 1
+#endif
+constexpr int SELL_PAIR = CPD_SELL_PAIR;
+__host__ __device__ __forceinline__ int64_t sell_pos(int64_t k, int64_t lane)
+{
+    return SELL_PAIR ? (k >> 1) * 64 + lane * 2 + (k & 1) : k * 32 + lane;
+}
 #ifndef CPD_PRE
 #define CPD_PRE 0   // 1: epilogue inputs held in registers across the sum (more registers)
 #endif
@@ -1019,18 +1030,33 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
 #pragma unroll
             for (int v = 0; v < NVEC; ++v) stg[v * 32 + lane] = vin[v] ? __ldcs(vin[v] + r) : 0.0;
 #endif
-        const int32_t* cp = M.col + b + lane;
-        const double* vp = M.val + b + lane;
+        const int32_t* cb = M.col + b;
+        const double* vb = M.val + b;
         double sm[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) sm[v] = (M.init && rl < M.rows) ? __ldcs(M.init + (int64_t)v * M.rows + rl) : 0.0;
         // two-stage software pipeline over rounds of SELL_U entries per lane
         auto ldround = [&](int (&cc)[SELL_U], double (&aa)[SELL_U], int k0) {
+            if constexpr (SELL_PAIR) {
+                static_assert(SELL_U % 2 == 0, "pair layout: even rounds");
 #pragma unroll
-            for (int u = 0; u < SELL_U; ++u) {
-                const bool ok = k0 + u < len;
-                cc[u] = ok ? ld_stream(cp + (int64_t)(k0 + u) * 32) : -1;
-                aa[u] = ok ? ld_stream(vp + (int64_t)(k0 + u) * 32) : 0.0;
+                for (int u = 0; u < SELL_U; u += 2) {
+                    const bool ok = k0 + u < len;   // len even: both of the pair
+                    const int64_t q = sell_pos(k0 + u, lane);
+                    const int2 c2 = ok ? __ldcs(reinterpret_cast<const int2*>(cb + q)) : make_int2(-1, -1);
+                    const double2 a2 = ok ? __ldcs(reinterpret_cast<const double2*>(vb + q)) : make_double2(0.0, 0.0);
+                    cc[u] = c2.x;
+                    cc[u + 1] = c2.y;
+                    aa[u] = a2.x;
+                    aa[u + 1] = a2.y;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < SELL_U; ++u) {
+                    const bool ok = k0 + u < len;
+                    cc[u] = ok ? ld_stream(cb + sell_pos(k0 + u, lane)) : -1;
+                    aa[u] = ok ? ld_stream(vb + sell_pos(k0 + u, lane)) : 0.0;
+                }
             }
         };
         int c[SELL_U];
@@ -1077,8 +1103,8 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
                 if (push_on) {   // a_ij x+_j into acc[i] for the short rows i of column j
                     const double xp = e.pushval(r);
                     for (int k = 0; k < len; ++k) {
-                        const int32_t cc = cp[(int64_t)k * 32];
-                        if (cc >= 0 && (cc & PUSH_BIT)) atomicAdd(&M.push[cc & COL_MASK], vp[(int64_t)k * 32] * xp);
+                        const int32_t cc = cb[sell_pos(k, lane)];
+                        if (cc >= 0 && (cc & PUSH_BIT)) atomicAdd(&M.push[cc & COL_MASK], vb[sell_pos(k, lane)] * xp);
                     }
                 }
             }

@@ -429,7 +429,7 @@ __global__ void k_sell_len(int32_t rows, int32_t nslice, const int32_t* p, int64
             if (j) col_range(j, lo, hi, c0, c1, lo, hi);
             mx = max(mx, hi - lo);
         }
-        len[s] = (int64_t)mx * 32;
+        len[s] = (int64_t)((mx + SELL_PAIR) / (1 + SELL_PAIR) * (1 + SELL_PAIR)) * 32;   // pair layout: even width
     }
 }
 
@@ -446,7 +446,7 @@ __global__ void k_sell_fill(int32_t rows, int32_t nslice, const int32_t* p, cons
         if (c1 > c0 && r < rows) col_range(j, lo, hi, c0, c1, lo, hi);
         const int64_t q0 = lo, n = hi - lo;
         for (int64_t k = 0; k < len; ++k) {
-            const int64_t d = b + k * 32 + lane;
+            const int64_t d = b + sell_pos(k, lane);
             scol[d] = k < n ? j[q0 + k] : -1;
             sval[d] = k < n ? x[q0 + k] : 0.0;
         }
