@@ -78,3 +78,20 @@ def test_no_gpu_fails_loudly():
     with pytest.raises(cpd.CpdError) as e:
         cpd.Problem.from_lp(lp)
     assert e.value.code == -6
+
+
+def test_corner_decide_host_only(golden):
+    """cpd_corner_decide (host only, reading D-4) on the hand cases, without a GPU."""
+    import oracle
+    for c in golden("corner_examples.json")["decide"]["cases"]:
+        assert cpd.corner_decide(c, c["m"]) == oracle.corner_decide(c, c["m"]) == (c["primal"], c["dual"])
+    with pytest.raises(cpd.CpdError):
+        cpd._check(cpd.lib().cpd_corner_decide(None, 1, None, None))
+
+
+def test_params_defaults_halpern_fields():
+    """cpd_params carries the NEXT-1 fields with their documented defaults (struct layout
+    shared with include/cpd.h)."""
+    p = cpd.cpd_params_default()
+    assert (p.method, p.reflection, p.pid, p.kp, p.ki, p.kd) == (0, 1.0, 0, 0.99, 0.01, 0.0)
+    assert (p.check_every, p.restart, p.use_graph) == (64, 1, 1)
