@@ -94,12 +94,13 @@ int cpd_problem_destroy(cpd_problem *p);
 /* m, n, nnz, number of long (split) rows in each layout's SpMV plan. */
 int cpd_problem_info(const cpd_problem *p, int64_t info[8]);
 /* Which SpMV engine paths the problem's plans use, for tests and
- * diagnostics: out[12] = {A warp plan (k_csrw) 1/0, A heavy rows (k_dense), A dense
+ * diagnostics: out[16] = {A warp plan (k_csrw) 1/0, A heavy rows (k_dense), A dense
  * column blocks, A column slabs of the long pieces, A short-row slab passes
  * (0 = off), A long rows, A long pieces, A rows items, A^T SELL-32 1/0, hot rows
- * (renumbered), A TMA plan entries (k_spmv), columns renumbered 1/0}.  Renumbering is
- * internal: every vector in or out of the ABI is in the caller's order. */
-int cpd_problem_plan_info(const cpd_problem *p, int64_t out[12]);
+ * (renumbered), A TMA plan entries (k_spmv), columns renumbered 1/0, fused hot rows
+ * (hot-row fusion: the primal step forms their dual-step products; 0 = off), 0, 0, 0}.
+ * Renumbering is internal: every vector in or out of the ABI is in the caller's order. */
+int cpd_problem_plan_info(const cpd_problem *p, int64_t out[16]);
 
 /* Solver parameters (every constant of the R-PDHG reading, §8(c)). */
 typedef struct {

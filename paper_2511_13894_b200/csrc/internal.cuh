@@ -74,6 +74,12 @@ struct Plan {
     DBuf<uint16_t> dense_col16;           // [nnz] column offset in the HB block of the heavy rows' entries
     DBuf<int32_t> dense_ptr;              // [nhb + 1] item range of each block
     int32_t dense_maxitems = 0;           // most items in one block (k_dense smem)
+    // hot-row fusion: rows 0..hotd-1 formed by the primal step; the fused dual step's
+    // dense items without them
+    int32_t hotd = 0;
+    DBuf<PlanEntry> dense_ent_f;
+    DBuf<int32_t> dense_ptr_f;
+    int32_t dense_maxitems_f = 0;
     // short rows by column slab (k_csrw slab mode): [nslab][rows + 1] pointers, entries slab-major
     int32_t short_on = 0;
     int32_t short_nslab = 1;
@@ -89,7 +95,7 @@ struct Plan {
 // rows x cols CSR with device column array d_col; long rows are cut into CAP pieces
 // at column-slab boundaries and their pieces ordered slab-major.
 void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rowptr, const int32_t* d_p,
-                const int32_t* d_col, const double* d_val, Plan& plan, bool warp = false);
+                const int32_t* d_col, const double* d_val, Plan& plan, bool warp = false, int32_t hotd_req = 0);
 
 // SELL-32 copy of a CSR layout whose rows are short and of similar length
 // (DESIGN.md §6): slices of 32 consecutive rows, each padded to its longest row,
@@ -102,6 +108,7 @@ struct Sell {
     int64_t padded = 0;
     int32_t r0 = 0, rows = 0;   // the rows [r0, r0 + rows) of the layout it holds
     int32_t c0 = 0, c1 = 0;     // c1 > c0: only their entries in columns [c0, c1)
+    bool rev = false;           // each lane's entries in descending column order
     bool on = false;
 };
 
@@ -134,7 +141,7 @@ struct Matrix {
 // SELL-32 of the short-row suffix of a warp-plan layout (rows sorted by length).
 void build_short_sell(Matrix& M, const std::vector<int32_t>& rp);
 // Build M.sell when the padded size is at most `max_ratio` x nnz (else M.sell.on = false).
-void build_sell(Matrix& M, int64_t nnz, double max_ratio);
+void build_sell(Matrix& M, int64_t nnz, double max_ratio, bool rev = false);
 
 }  // namespace cpd
 
@@ -217,6 +224,8 @@ namespace cpd {
 
 // Per-stream execution context: control block, reduction scratch, long-row
 // scratch for both layouts.
+bool fuse_ok(const cpd_problem* P);   // hot-row fusion applies (solver.cu)
+
 struct Ctx {
     const cpd_problem* P = nullptr;
     cudaStream_t st = nullptr;
@@ -237,6 +246,9 @@ struct Ctx {
     DBuf<double> shortA, shortAT;     // running row sums of the short-row slab passes
     DBuf<double> sshortA;             // running row sums of the short-row SELL half passes
     double* push_acc = nullptr;       // set around the primal/dual pair of a batch (short-row push)
+    DBuf<double> hotpart;             // hot-row fusion: per-warp partials [hotd][hot_stride]
+    int32_t hot_stride = 0;
+    bool fuse = false;                // set around the primal/dual pair of a batch (hot-row fusion)
     DBuf<double> red;                 // this rank's totals of the last reduction (distributed)
     DBuf<double> part, recv;          // reduce-scatter send [world][2][L] / receive [2][L] buffers
     // fused split product (CPD_P2P=1): symmetric receive window [world][2][L] and the
@@ -252,6 +264,7 @@ struct Ctx {
     explicit Ctx(const cpd_problem* p);
     ~Ctx();
     DevPlan planA() const;
+    DevPlan planA_fused() const;
     DevPlan planAT() const;
     void pull_ctl();                                   // D2H of the control block + sync
     void set_i64(int64_t* dev_field, int64_t v);

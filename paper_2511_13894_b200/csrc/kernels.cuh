@@ -71,7 +71,17 @@ constexpr int DCHUNK = CPD_DCHUNK;   // k_dense: entries per item (balances the 
 constexpr int TPB_D = CPD_TPB_D;
 constexpr int FIN_SPLIT = 1024;
 constexpr int TPB_F = 256;       // k_finish threads per CTA (1024 measured slower: 52 vs 45 us)
-constexpr int HOT_ROWS = 4096;   // y entries of the longest rows of A staged in k_sell's shared memory  // k_finish: rows with more partials get a CTA, the rest a warp
+constexpr int HOT_ROWS = 4096;
+#ifndef CPD_HOTY_FUSED
+#define CPD_HOTY_FUSED 2048
+#endif
+constexpr int HOT_ROWS_FUSED = CPD_HOTY_FUSED;   // staged y entries of the fused primal step (smem budget)
+#ifndef CPD_HOTY
+#define CPD_HOTY 2048
+#endif
+// staged y entries of the other A^T SELL passes (C5: 4096 halves the two-vector check
+// pass's occupancy, 1.90 vs 0.95 ms — profiles/r02_kernel_iterations.md)
+constexpr int HOT_ROWS_STAGED = CPD_HOTY;   // y entries of the longest rows of A staged in k_sell's shared memory  // k_finish: rows with more partials get a CTA, the rest a warp
 
 enum { MODE_FULL = 0, MODE_PRIMAL_ONLY = 1, MODE_NONE = 2, MODE_DUAL_ONLY = 3 };
 enum { ST_RUNNING = -1, ST_CONVERGED = 0, ST_ITER_LIMIT = 1, ST_TIME_LIMIT = 2, ST_FAIL = 3 };
@@ -104,6 +114,10 @@ struct DevPlan {
     const int32_t* long_ents;  // k_finish order: nfin_heavy rows (a CTA each), then the rest (a warp each)
     int32_t nfin_heavy;
     double* lpart;             // [pieces * GW * 2] warp partial sums (NV <= 2)
+    // fused dual step (hot-row fusion): long rows l < hotd (= internal rows 0..hotd-1)
+    // are summed from the primal step's per-warp partials hot_part[l * hot_stride + w]
+    int32_t hotd = 0, hot_stride = 0;
+    const double* hot_part = nullptr;
 };
 
 struct DevCsr {
@@ -865,6 +879,23 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
         double sm[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) sm[v] = 0.0;
+        if (NV == 1 && l < P.hotd) {   // fused: the primal step's per-warp partials of this row
+            double a8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const double* hp = P.hot_part + (int64_t)l * P.hot_stride;
+            int t = threadIdx.x;
+            for (; t + 7 * TPB_F < P.hot_stride; t += 8 * TPB_F)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a8[u] += __ldcg(hp + t + u * TPB_F);
+            for (; t < P.hot_stride; t += TPB_F) a8[0] += __ldcg(hp + t);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sm[0] += a8[q];
+            block_sum<NV, TPB_F>(sm, s_w);
+            if (threadIdx.x == 0) {
+                const int r = P.long_row[l];
+                e.row(r, sm, vin, r, acc);
+            }
+            continue;
+        }
         const int64_t t0 = (int64_t)P.long_ptr[l] * P.pslot, t1 = (int64_t)P.long_ptr[l + 1] * P.pslot;
         // 8 independent accumulators per thread (loads in flight), combined in fixed order
         double a8[8][NV];
@@ -946,7 +977,17 @@ struct DevSell {
     // sums in part[v * rows + rl] and skips the epilogue; the second starts from init
     double* part = nullptr;
     const double* init = nullptr;
+    // hot-row fusion (the primal step): each lane holds its padding first,
+    // then its entries in DESCENDING row order, so the hot rows 0..hotd-1 are each lane's
+    // last entries and sit in the slice's final round; a_hj x+_j is accumulated per lane
+    // in shared memory and flushed as per-warp partials hot_part[h * hot_stride + warp]
+    int32_t hotd = 0, hot_stride = 0;
+    double* hot_part = nullptr;
 };
+template <class E, class = void>
+struct FuseRole { static constexpr int v = 0; };   // 1: primal step (forms the hot sums), 2: dual step
+template <class E>
+struct FuseRole<E, std::void_t<decltype(E::FUSE)>> { static constexpr int v = E::FUSE; };
 
 constexpr int TPB_SELL = 256;
 // SELL entry layout inside a slice: SELL_PAIR = 1 stores entries k, k+1 of a lane next to
@@ -971,7 +1012,7 @@ constexpr int SELL_U = CPD_SELL_U;   // entries per lane in flight
 #ifndef CPD_SELL_MINB
 #define CPD_SELL_MINB 4
 #endif
-template <int NV, class Epi>
+template <int NV, class Epi, int FZ = 0>   // FZ: the fused primal step (hot-row fusion)
 __global__ void __launch_bounds__(TPB_SELL, CPD_SELL_MINB)
 k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr,
        double* red, int prev, int fin)
@@ -999,12 +1040,18 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
     const int nw = gridDim.x * (TPB_SELL / 32);
     __shared__ double vst[TPB_SELL / 32][(NVEC > 0 ? NVEC : 1) * 32];
     // the gathered vector's hot prefix (the longest rows of A, most of the gathers)
-    extern __shared__ __align__(16) double yhot[];   // [NV][hot]
+    extern __shared__ __align__(16) double yhot[];   // [NV][hot], then the fused rows' accumulators
     const int hot = M.hot;
     for (int t = threadIdx.x; t < hot; t += TPB_SELL) {
         yhot[t] = v0[t];
         if (NV > 1) yhot[hot + t] = v1[t];
     }
+    // hot-row fusion: this warp's lane-private accumulators hacc[h][lane] (conflict-free,
+    // fixed summation order: the warp's slices in order, then a fixed lane tree)
+    constexpr bool FUSE = FZ && FuseRole<Epi>::v == 1 && NV == 1;
+    const int hotd = FUSE ? M.hotd : 0;
+    double* hacc = yhot + NV * hot + (threadIdx.x >> 5) * (hotd * 32);
+    for (int h = 0; h < hotd; ++h) hacc[h * 32 + lane] = 0.0;
     __syncthreads();
     // push only for an iteration the dual step will complete (k < k_stop)
     const bool push_on = M.push != nullptr && ctl->k < ctl->k_stop;
@@ -1062,7 +1109,7 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
         int c[SELL_U];
         double a[SELL_U];
         ldround(c, a, 0);
-        for (int k0 = 0; k0 < len; k0 += SELL_U) {
+        auto round_sum = [&]() {   // this round's gathers and products
             double g[SELL_U], g2[SELL_U];
 #pragma unroll
             for (int u = 0; u < SELL_U; ++u) {
@@ -1070,19 +1117,31 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
                 g[u] = c[u] < 0 ? 0.0 : cc < hot ? yhot[cc] : __ldg(&v0[cc]);
                 if (NV > 1) g2[u] = c[u] < 0 ? 0.0 : cc < hot ? yhot[hot + cc] : __ldg(&v1[cc]);
             }
+            return [=, &sm](void) {
+#pragma unroll
+                for (int u = 0; u < SELL_U; ++u)
+                    if (c[u] >= 0) {
+                        sm[0] += a[u] * g[u];
+                        if (NV > 1) sm[NV - 1] += a[u] * g2[u];
+                    }
+            };
+        };
+        // all but the last round: the next round's loads in flight during this round's
+        // gathers; the last round's entries stay in c / a (the fused primal step uses them)
+        int k0 = 0;
+        for (; k0 + SELL_U < len; k0 += SELL_U) {
+            auto fma = round_sum();
             int cn[SELL_U];
             double an[SELL_U];
             ldround(cn, an, k0 + SELL_U);
+            fma();
 #pragma unroll
             for (int u = 0; u < SELL_U; ++u) {
-                if (c[u] >= 0) {
-                    sm[0] += a[u] * g[u];
-                    if (NV > 1) sm[NV - 1] += a[u] * g2[u];
-                }
                 c[u] = cn[u];
                 a[u] = an[u];
             }
         }
+        if (len > 0) round_sum()();
         if (M.part) {   // first column pass: running sums only
             if (rl < M.rows)
 #pragma unroll
@@ -1098,7 +1157,35 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
 #endif
                 vs[v] = stg + v * 32;
             }
-            e.row(r, sm, vs, lane, acc);
+            if constexpr (FUSE) {
+                const double xp = e.row(r, sm, vs, lane, acc);
+                if (hotd > 0) {
+                    // the last round holds the lane's last (= lowest-row) entries (padding
+                    // comes first in a reversed slice)
+                    bool more = len > SELL_U;
+#pragma unroll
+                    for (int u = 0; u < SELL_U; ++u) {
+                        const int32_t cc = c[u] & COL_MASK;
+                        const bool hit = c[u] >= 0 && cc < hotd;
+                        if (hit) hacc[cc * 32 + lane] += a[u] * xp;
+                        // an earlier hot entry only if the round starts with one
+                        if (u == 0) more = more && hit;
+                    }
+                    if (__any_sync(__activemask(), more)) {   // rare: scan back from the last round
+                        for (int k = len - SELL_U - 1; k >= 0; --k) {
+                            const int32_t c0 = more ? __ldg(cb + sell_pos(k, lane)) : 0;
+                            const int32_t cc = c0 & COL_MASK;
+                            if (more) {
+                                if (c0 >= 0 && cc < hotd) hacc[cc * 32 + lane] += __ldg(vb + sell_pos(k, lane)) * xp;
+                                else more = false;   // padding or a colder row: no hot entry before it
+                            }
+                            if (!__any_sync(__activemask(), more)) break;
+                        }
+                    }
+                }
+            } else {
+                e.row(r, sm, vs, lane, acc);
+            }
             if constexpr (PushRole<Epi>::v == 1) {
                 if (push_on) {   // a_ij x+_j into acc[i] for the short rows i of column j
                     const double xp = e.pushval(r);
@@ -1108,6 +1195,15 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
                     }
                 }
             }
+        }
+    }
+    if constexpr (FUSE) {   // per-warp partials of the hot rows (fixed-order lane tree)
+        const int gw = blockIdx.x * (TPB_SELL / 32) + (threadIdx.x >> 5);
+        for (int h = 0; h < hotd; ++h) {
+            double v = hacc[h * 32 + lane];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) M.hot_part[(int64_t)h * M.hot_stride + gw] = v;
         }
     }
     if (M.part) return;   // first column pass: no epilogue, no partials
@@ -1590,6 +1686,7 @@ struct EpiPrimalT {
     static constexpr int NS = 5;   // c^T x_k, ||r_D(y_k)||^2, bound terms, #nonfinite(x_{k+1}), #{|r_D_j| > eps}
     static constexpr int NVEC = PE ? 5 : 3;
     static constexpr int PUSH = 1;
+    static constexpr int FUSE = 1;
     __device__ __forceinline__ double pushval(int j) const { return xn[j]; }
     const double* c;
     Bounds bd;
@@ -1616,8 +1713,8 @@ struct EpiPrimalT {
         return v == 0 ? c : v == 1 ? xc : v == 2 ? xac : v == 3 ? bd.l : bd.u;
     }
     // row j of A^T; vin[v][li] = staged (or global, li = j) input v of row j
-    __device__ __forceinline__ void row(int j, const double* s, const double* const* vin, int li,
-                                        double* acc) const
+    __device__ __forceinline__ double row(int j, const double* s, const double* const* vin, int li,
+                                          double* acc) const
     {
         const double cj = vin[0][li];
         const double z = cj - s[0];
@@ -1636,6 +1733,7 @@ struct EpiPrimalT {
         const double rd = dual_terms(z, lo, hi, acc[1], acc[2], w ? w[j] : 1.0);
         acc[3] += isfinite(xp) ? 0.0 : 1.0;
         acc[4] += fabs(rd) > eps_dual ? 1.0 : 0.0;
+        return xp;
     }
     // F(k): termination of iterate k (k >= 1, not a check iteration), P:124-126 / P:391-395.
     __device__ void finalize(const double* tot, Ctl* ctl) const
@@ -1667,6 +1765,7 @@ struct EpiDual {
     static constexpr int NS = 3;   // ||b - A x_{k+1}||^2, b^T y_{k+1}, #nonfinite(y_{k+1})
     static constexpr int NVEC = 4;
     static constexpr int PUSH = 2;
+    static constexpr int FUSE = 2;
     const double* b;
     double *y, *ya, *ax;
     double sigma, inv_t;

@@ -3,6 +3,7 @@
 // The problem statement is P:64-92 (A m x n, b, c, bounds handled implicitly).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -37,6 +38,9 @@ static int64_t slab_cols() { return env_i64("CPD_SLAB_COLS", SLAB_COLS); }
 static int64_t heavy_min() { return env_i64("CPD_HEAVY_MIN", HEAVY_MIN); }
 #ifndef CPD_SLAB_MIN
 #define CPD_SLAB_MIN 0   // long rows shorter than this are not cut at column-slab boundaries
+#endif
+#ifndef CPD_HOTD_DEFAULT
+#define CPD_HOTD_DEFAULT 6   // hot-row fusion: the longest rows whose dual-step product the primal step forms
 #endif
 #ifndef CPD_SHORT_SLABS
 #define CPD_SHORT_SLABS 2   // short rows (CPD_SHORT=1): column slabs of n / 2 (80 MB of C5's x each)
@@ -153,7 +157,7 @@ __global__ void k_short_fill(int32_t rows, int32_t nslab, int64_t long_min, cons
 // (while the CTAs sweep one slab, that slab of the gathered vector stays in L2);
 // k_finish sums its pieces and applies its epilogue.
 void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, const int32_t* d_p,
-                const int32_t* d_col, const double* d_val, Plan& plan, bool warp)
+                const int32_t* d_col, const double* d_val, Plan& plan, bool warp, int32_t hotd_req)
 {
     // TMA plan: <= RMAX rows / CAP nnz per entry, rows > SINGLE_MIN long, CAP pieces.
     // warp plan (k_csrw): <= 32 rows / WCAP_ROWS nnz per item, rows > WLONG long, WCAP_LONG pieces.
@@ -304,6 +308,31 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
         plan.dense_ptr.alloc(nhb + 1);
         CPD_CUDA(cudaMemcpy(plan.dense_ent.p, dent.data(), sizeof(PlanEntry) * dent.size(), cudaMemcpyHostToDevice));
         CPD_CUDA(cudaMemcpy(plan.dense_ptr.p, dptr.data(), sizeof(int32_t) * (nhb + 1), cudaMemcpyHostToDevice));
+        // hot-row fusion: rows 0..D-1 (the longest, heavy, long-row ids 0..D-1) take their
+        // dual-step product from the primal step; the fused dual step's dense items skip them
+        int32_t D = 0;
+        while (D < hotd_req && D < nl && lrows[D] == D && is_heavy[D]) ++D;
+        plan.hotd = D;
+        if (D > 0) {
+            std::vector<PlanEntry> fent;
+            std::vector<int32_t> fptr(nhb + 1, 0);
+            int32_t fmax = 1;
+            const int32_t hot_slot_end = lptr[D];   // slots of long rows 0..D-1 come first
+            for (int32_t b = 0; b < nhb; ++b) {
+                int32_t c = 0;
+                for (const PlanEntry& E : dl[b])
+                    if (E.a >= hot_slot_end) { fent.push_back(E); ++c; }
+                fptr[b + 1] = (int32_t)fent.size();
+                fmax = std::max(fmax, c);
+            }
+            plan.dense_maxitems_f = fmax;
+            plan.dense_ent_f.alloc(std::max<size_t>(fent.size(), 1));
+            plan.dense_ptr_f.alloc(nhb + 1);
+            if (!fent.empty())
+                CPD_CUDA(cudaMemcpy(plan.dense_ent_f.p, fent.data(), sizeof(PlanEntry) * fent.size(),
+                                    cudaMemcpyHostToDevice));
+            CPD_CUDA(cudaMemcpy(plan.dense_ptr_f.p, fptr.data(), sizeof(int32_t) * (nhb + 1), cudaMemcpyHostToDevice));
+        }
     }
     std::vector<int32_t> next(lptr.begin(), lptr.end() - 1);
     int64_t npieces = 0;
@@ -386,11 +415,13 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
     {
         const int64_t ps = warp ? 1 : GW;
         std::vector<int32_t> order;
+        // (the fused hot rows always get a CTA: their sums span the primal step's warps)
+        auto cta = [&](int32_t l) { return l < plan.hotd || (int64_t)(lptr[l + 1] - lptr[l]) * ps > FIN_SPLIT; };
         for (int32_t l = 0; l < nl; ++l)
-            if ((int64_t)(lptr[l + 1] - lptr[l]) * ps > FIN_SPLIT) order.push_back(l);
+            if (cta(l)) order.push_back(l);
         plan.nfin_heavy = (int32_t)order.size();
         for (int32_t l = 0; l < nl; ++l)
-            if ((int64_t)(lptr[l + 1] - lptr[l]) * ps <= FIN_SPLIT) order.push_back(l);
+            if (!cta(l)) order.push_back(l);
         plan.long_ents.alloc(std::max(nl, 1));
         if (nl) CPD_CUDA(cudaMemcpy(plan.long_ents.p, order.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice));
     }
@@ -433,10 +464,11 @@ __global__ void k_sell_len(int32_t rows, int32_t nslice, const int32_t* p, int64
     }
 }
 
-// one thread per (slice, lane): row r0 + r's entries, then padding (-1, 0.0)
+// one thread per (slice, lane): row r0 + r's entries, then padding (-1, 0.0); rev: the
+// padding, then the row's entries in descending column order
 __global__ void k_sell_fill(int32_t rows, int32_t nslice, const int32_t* p, const int32_t* j, const double* x,
                             const int64_t* sp, int32_t* scol, double* sval, int32_t r0 = 0, int32_t c0 = 0,
-                            int32_t c1 = 0)
+                            int32_t c1 = 0, bool rev = false)
 {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)nslice * 32;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -447,8 +479,13 @@ __global__ void k_sell_fill(int32_t rows, int32_t nslice, const int32_t* p, cons
         const int64_t q0 = lo, n = hi - lo;
         for (int64_t k = 0; k < len; ++k) {
             const int64_t d = b + sell_pos(k, lane);
-            scol[d] = k < n ? j[q0 + k] : -1;
-            sval[d] = k < n ? x[q0 + k] : 0.0;
+            // rev: padding first, then the entries in reverse order (each lane's last
+            // entries are its lowest columns, in the slice's last round)
+            const int64_t kk = rev ? k - (len - n) : k;
+            const bool ok = rev ? kk >= 0 : k < n;
+            const int64_t q = q0 + (rev ? n - 1 - kk : k);
+            scol[d] = ok ? j[q] : -1;
+            sval[d] = ok ? x[q] : 0.0;
         }
     }
 }
@@ -488,8 +525,9 @@ void mark_push(cpd_problem* P)
 
 // SELL-32 of rows [r0, r0 + rows) of M's CSR into S (S.on = false when padding > max_ratio).
 static void build_sell_rows(const Matrix& M, Sell& S, int32_t r0, int32_t rows, int64_t nnz, double max_ratio,
-                            int32_t c0 = 0, int32_t c1 = 0)
+                            int32_t c0 = 0, int32_t c1 = 0, bool rev = false)
 {
+    S.rev = rev;
     S.c0 = c0;
     S.c1 = c1;
     S.on = false;
@@ -517,16 +555,18 @@ static void build_sell_rows(const Matrix& M, Sell& S, int32_t r0, int32_t rows, 
     S.col.alloc((size_t)std::max<int64_t>(padded, 1));
     S.val.alloc((size_t)std::max<int64_t>(padded, 1));
     const int g2 = (int)std::min<int64_t>(((int64_t)ns * 32 + 255) / 256, 65536);
-    k_sell_fill<<<g2, 256>>>(rows, ns, M.p.p, M.j.p, M.x.p, S.sp.p, S.col.p, S.val.p, r0, c0, c1);
+    k_sell_fill<<<g2, 256>>>(rows, ns, M.p.p, M.j.p, M.x.p, S.sp.p, S.col.p, S.val.p, r0, c0, c1, rev);
     CPD_CUDA(cudaGetLastError());
     CPD_CUDA(cudaDeviceSynchronize());
     S.nslice = ns;
     S.on = true;
 }
 
-void build_sell(Matrix& M, int64_t nnz, double max_ratio)
+// rev: each lane's entries in descending column order (A^T of a renumbered problem: the
+// hot rows of A, its lowest columns, become each lane's last entries — hot-row fusion)
+void build_sell(Matrix& M, int64_t nnz, double max_ratio, bool rev)
 {
-    build_sell_rows(M, M.sell, 0, M.rows, nnz, max_ratio);
+    build_sell_rows(M, M.sell, 0, M.rows, nnz, max_ratio, 0, 0, rev);
 }
 
 // Short rows of a warp-plan layout whose rows are ordered by decreasing length (hot-row
@@ -746,6 +786,18 @@ static void renumber(cpd_problem* P, std::vector<int32_t>& hp)
         P->AT.x = std::move(nx);
     }
     k_remap<<<grid(nnz), 256>>>(nnz, P->AT.j.p, rpinv.p);
+    {   // each row of A^T in ascending new row order (A^T's SELL reverses it: hot-row fusion)
+        DBuf<int32_t> sj(std::max<int64_t>(nnz, 1));
+        DBuf<double> sx(std::max<int64_t>(nnz, 1));
+        size_t tb = 0;
+        CPD_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, P->AT.j.p, sj.p, P->AT.x.p, sx.p, nnz, n,
+                                                     P->AT.p.p, P->AT.p.p + 1));
+        DBuf<unsigned char> tmp(std::max<size_t>(tb, 1));
+        CPD_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, P->AT.j.p, sj.p, P->AT.x.p, sx.p, nnz, n,
+                                                     P->AT.p.p, P->AT.p.p + 1));
+        P->AT.j = std::move(sj);
+        P->AT.x = std::move(sx);
+    }
     // CSR(A) = the stable transpose: new rows, ascending new columns
     transpose(n, m, nnz, P->AT.p.p, P->AT.j.p, P->AT.x.p, P->A.p.p, P->A.j.p, P->A.x.p, sms);
     // vectors in the new orders
@@ -1059,7 +1111,7 @@ void scale_problem(cpd_problem* P, int32_t ruiz_iters, int32_t pc)
     CPD_CUDA(cudaGetLastError());
     P->uniform_bounds = false;
     // derived copies of the values
-    if (P->AT.sell.on) build_sell(P->AT, P->nnz, 1.25);
+    if (P->AT.sell.on) build_sell(P->AT, P->nnz, 1.25, P->AT.sell.rev);
     if (P->A.sell.on) build_sell(P->A, P->nnz, 1.25);
     if (P->A.sell_short.on) {   // the scaled values of the short-row suffix
         const int32_t r0 = P->A.sell_short.r0, nr = P->A.sell_short.rows;
@@ -1223,7 +1275,11 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         }
         bool warpA = 4 * long_nnz >= nnz && nnz > 0;
         if (we) warpA = we[0] != '0';
-        build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.x.p, P->A.plan, warpA);
+        // hot-row fusion of the top rows into the primal step (renumbered problems;
+        // env CPD_HOTD = rows, 0 disables; default CPD_HOTD_DEFAULT)
+        const char* hde = getenv("CPD_HOTD");
+        const int32_t hotd_req = P->hot > 0 ? (hde ? atoi(hde) : CPD_HOTD_DEFAULT) : 0;
+        build_plan(m, n, hp, P->A.p.p, P->A.j.p, P->A.x.p, P->A.plan, warpA, hotd_req);
         build_short_sell(P->A, hp);
         tm.mark("plan A");
         // SELL-32 where the rows are short and even (padding <= 25%); CPD_SELL=0 disables
@@ -1231,7 +1287,7 @@ cpd_problem* cpd_problem_create_impl(int32_t m, int32_t n, int64_t nnz, const in
         const bool sell_ok = !(se && se[0] == '0');
         // (A^T only: for A the dual epilogue's four staged vectors favour the TMA plan
         // kernel, measured on C4 — profiles/r01_kernel_iterations.md)
-        if (sell_ok && nnz <= (int64_t)n * 64) build_sell(P->AT, nnz, 1.25);
+        if (sell_ok && nnz <= (int64_t)n * 64) build_sell(P->AT, nnz, 1.25, P->hot > 0);
         tm.mark("sell");
         // every A^T pass runs on SELL when it is on: its TMA plan is only needed otherwise
         if (!P->AT.sell.on) {

@@ -66,6 +66,11 @@ Ctx::Ctx(const cpd_problem* p) : P(p)
     lpartAT.alloc((size_t)std::max<int64_t>(1, pt.long_pieces) * GW * 2);
     if (pa.short_on) shortA.alloc((size_t)2 * p->A.rows);
     if (p->A.sell_half[0].on) sshortA.alloc((size_t)2 * p->A.sell_half[0].rows);
+    if (fuse_ok(p)) {   // per-warp partials of the fused hot rows; slots never written stay 0
+        hot_stride = 64 * p->num_sms;   // >= the primal step's warps (<= 64 resident per SM)
+        hotpart.alloc((size_t)pa.hotd * hot_stride);
+        CPD_CUDA(cudaMemset(hotpart.p, 0, sizeof(double) * (size_t)pa.hotd * hot_stride));
+    }
     if (pt.short_on) shortAT.alloc((size_t)2 * p->AT.rows);
     red.alloc(NSMAX);
     CPD_CUDA(cudaMemset(red.p, 0, sizeof(double) * NSMAX));
@@ -97,6 +102,29 @@ DevPlan Ctx::planA() const
                    pl.dense_ptr.p, pl.dense_col16.p, pl.dense_maxitems, pl.short_ptr.p, pl.short_col.p, pl.short_val.p, shortA.p, nullptr,
                    pl.long_row.p,
                    pl.long_ptr.p, pl.long_ents.p, pl.nfin_heavy, lpartA.p};
+}
+
+// Hot-row fusion applies to single-GPU problems whose A^T passes run on a reversed
+// SELL-32 and whose plan fused rows; not with the short-row push.
+// CPD_FUSE=0 disables it at solve time.
+bool fuse_ok(const cpd_problem* P)
+{
+    const char* e = getenv("CPD_FUSE");
+    return P->A.plan.hotd > 0 && P->AT.sell.on && P->AT.sell.rev && !P->push_on && P->split < 0 &&
+           !(e && e[0] == '0');
+}
+
+DevPlan Ctx::planA_fused() const
+{
+    DevPlan d = planA();
+    const Plan& pl = P->A.plan;
+    d.dense_ent = pl.dense_ent_f.p;
+    d.dense_ptr = pl.dense_ptr_f.p;
+    d.dense_maxitems = pl.dense_maxitems_f;
+    d.hotd = pl.hotd;
+    d.hot_stride = hot_stride;
+    d.hot_part = hotpart.p;
+    return d;
 }
 
 DevPlan Ctx::planAT() const
@@ -144,7 +172,7 @@ static std::mutex g_grid_mu;
 
 // Resident-CTA grid of `kernel` at (threads, dynamic smem) on the CURRENT device,
 // cached per (device, kernel, smem).  The max-dynamic-smem attribute is per device,
-// so it is set (once) on every device a kernel runs on.
+// so it is set on every device a kernel runs on (raised to the largest size seen).
 static int occ_grid(const void* kernel, int threads, size_t smem, int num_sms, int cap_per_sm = 0)
 {
     int dev = 0;
@@ -154,8 +182,13 @@ static int occ_grid(const void* kernel, int threads, size_t smem, int num_sms, i
     const auto key = std::make_tuple(dev, kernel, smem, threads);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
-    if (smem > 0)
+    // the attribute only ever grows (a launch of an earlier, larger size stays valid)
+    static std::map<std::pair<int, const void*>, size_t> attr;
+    size_t& cur = attr.try_emplace(std::make_pair(dev, kernel), (size_t)0).first->second;
+    if (smem > cur) {
         CPD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cur = smem;
+    }
     int nb = 0;
     CPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem));
     nb = std::max(1, nb);
@@ -174,14 +207,28 @@ void launch_spmv(Ctx& cx, const Matrix& M, const DevPlan& dp, VecSel v0, VecSel 
 {
     if (M.sell.on) {
         // A^T gathers y: its hot prefix (hot-row renumbering) is staged in shared memory
-        const int hot = (&M == &cx.P->AT) ? cx.P->hot : 0;
-        const size_t hsm = (size_t)NV * hot * sizeof(double);
-        const int sgrid = occ_grid((const void*)k_sell<NV, Epi>, TPB_SELL, hsm, cx.P->num_sms);
+        // fused primal step: per-lane accumulators of the hot rows after the staged y
+        constexpr bool FZ = FuseRole<Epi>::v == 1 && NV == 1;
+        const bool fz = FZ && cx.fuse && &M == &cx.P->AT;
+        const int hotd = fz ? cx.P->A.plan.hotd : 0;
+        const int hot = (&M == &cx.P->AT) ? std::min(cx.P->hot, fz ? HOT_ROWS_FUSED : HOT_ROWS_STAGED) : 0;
+        const size_t hsm = (size_t)NV * hot * sizeof(double) + (size_t)(TPB_SELL / 32) * hotd * 32 * sizeof(double);
+        const void* kfn = fz ? (const void*)k_sell<NV, Epi, FZ ? 1 : 0> : (const void*)k_sell<NV, Epi, 0>;
+        const int sgrid = occ_grid(kfn, TPB_SELL, hsm, cx.P->num_sms);
         const int gr = std::max(1, std::min<int>(sgrid, (M.sell.nslice + 7) / 8));
         DevSell ds = M.dsell();
         ds.hot = hot;
+        if (fz) {
+            ds.hotd = hotd;
+            ds.hot_stride = cx.hot_stride;
+            ds.hot_part = cx.hotpart.p;
+        }
         if (PushRole<Epi>::v == 1) ds.push = cx.push_acc;
-        k_sell<NV, Epi><<<gr, TPB_SELL, hsm, cx.st>>>(ds, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p, red, 0, 1);
+        if (fz)
+            k_sell<NV, Epi, FZ ? 1 : 0><<<gr, TPB_SELL, hsm, cx.st>>>(ds, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p,
+                                                                    red, 0, 1);
+        else
+            k_sell<NV, Epi, 0><<<gr, TPB_SELL, hsm, cx.st>>>(ds, v0, v1, epi, g, cx.ctl, cx.bpart.p, cx.ctr.p, red, 0, 1);
         CPD_CUDA(cudaGetLastError());
         ++cx.launches;
         return;
@@ -348,7 +395,8 @@ static void pass(Ctx& cx, int side, VecSel v0, VecSel v1, const Epi& epi, Gate g
 {
     const cpd_problem* P = cx.P;
     const Matrix& M = side ? P->AT : P->A;
-    const DevPlan dp = side ? cx.planAT() : cx.planA();
+    const DevPlan dp = side ? cx.planAT()
+                            : ((FuseRole<Epi>::v == 2 && NV == 1 && cx.fuse) ? cx.planA_fused() : cx.planA());
     if (P->split < 0) {
         launch_spmv<NV>(cx, M, dp, v0, v1, epi, g, nullptr);
         return;
@@ -903,6 +951,7 @@ struct cpd_solver {
             rec(ev1, NODE_RESTART);
         }
         cx.push_acc = ACC.p;   // primal step pushes short-row products, dual step consumes them
+        cx.fuse = fuse_ok(P);  // primal step forms the hot rows' dual-step products
         for (int s = 0; s < K; ++s) {
             const int n1 = NODE_K0 + 2 * s, n2 = n1 + 1;
             const Gate g1{GATE_K1, s, n1, active.p}, g2{GATE_K2, s, n2, active.p};
@@ -931,6 +980,7 @@ struct cpd_solver {
             rec(ev1, n2);
         }
         cx.push_acc = nullptr;
+        cx.fuse = false;
         if (capture) graph_kernels[kind] = cx.launches - l0;
         CPD_CUDA(cudaMemcpyAsync(h_active, active.p, sizeof(int32_t) * nnodes, cudaMemcpyDeviceToHost, cx.st));
         CPD_CUDA(cudaMemcpyAsync(cx.h_ctl, cx.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, cx.st));
@@ -1591,7 +1641,7 @@ int cpd_problem_info(const cpd_problem* p, int64_t info[8])
     ABI_END
 }
 
-int cpd_problem_plan_info(const cpd_problem* p, int64_t out[12])
+int cpd_problem_plan_info(const cpd_problem* p, int64_t out[16])
 {
     ABI_BEGIN
     if (!p || !out) return fail(CPD_E_ARG, "NULL argument");
@@ -1608,6 +1658,8 @@ int cpd_problem_plan_info(const cpd_problem* p, int64_t out[12])
     out[9] = p->hot;
     out[10] = pl.warp ? 0 : pl.nent;
     out[11] = p->cperm.p ? 1 : 0;
+    out[12] = cpd::fuse_ok(p) ? pl.hotd : 0;
+    out[13] = out[14] = out[15] = 0;
     ABI_END
 }
 

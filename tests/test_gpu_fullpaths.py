@@ -167,3 +167,67 @@ def test_short_row_sell_modes(mode, monkeypatch):
     _, _, ro = oracle.solve(olp, oracle.default_params(max_iters=2000))
     assert r["status"] == ro["status"] and r["iterations"] == ro["iterations"]
     assert r["pobj"] == pytest.approx(ro["pobj"], rel=1e-6)
+
+
+@pytest.mark.parametrize("hotd", ["0", "1", "3", "6", "16"])
+def test_hot_row_fusion_lockstep(hotd, monkeypatch):
+    """Hot-row fusion: the primal step forms A x+ of the longest rows from
+    per-lane shared-memory accumulators over the last entries of each lane (A^T's SELL
+    lanes hold their entries in descending row order; earlier hot entries are re-read),
+    the fused dual step sums the per-warp partials instead of running k_dense on those
+    rows.  Off, one, three, six (the default) and sixteen rows (> one SELL round of
+    entries per lane: the re-read path) — 1e-9 lockstep over 1000 iterations with
+    restarts (check passes use the unfused plan), graph vs eager bit-identical (the
+    fused sums are in a fixed order), termination objective vs the oracle."""
+    for k, v in FORCE.items():
+        monkeypatch.setenv(k, v)
+    monkeypatch.setenv("CPD_HOTD", hotd)
+    lp = lpgen.config("c5-s")
+    olp = oracle.OracleLP(lp)
+    P = cpd.Problem.from_lp(lp)
+    pi = P.plan_info()
+    assert pi["fused_rows"] == min(int(hotd), pi["heavy_rows"]), pi
+    if hotd == "16":
+        assert pi["fused_rows"] > 6, pi
+    eta = 0.9 / oracle.power_sigma(olp)
+    S = cpd.Solver(P, step_size=eta, restart=1)
+    R = oracle.Run(olp, oracle.default_params(step_size=eta, restart=1), mode=oracle.MODE_NONE)
+    k = 0
+    for target in (1, 2, 64, 65, 300, 1000):
+        S.step(target - k)
+        R.run(target - k)
+        k = target
+        xg, yg = S.get_iterate()
+        xo, yo = R.get()
+        assert close(xg, xo) and close(yg, yo), (hotd, k, worst(xg, xo), worst(yg, yo))
+    a = cpd.Solver(P, max_iters=700, use_graph=1)
+    b = cpd.Solver(P, max_iters=700, use_graph=0)
+    ra, rb = a.solve(), b.solve()
+    assert ra["iterations"] == rb["iterations"] == 700
+    xa, ya = a.get_iterate()
+    xb, yb = b.get_iterate()
+    assert np.array_equal(xa, xb) and np.array_equal(ya, yb)
+    _, _, ro = oracle.solve(olp, oracle.default_params(max_iters=700))
+    assert ra["status"] == ro["status"] and ra["pobj"] == pytest.approx(ro["pobj"], rel=1e-6)
+
+
+def test_hot_row_fusion_solve_time_switch(forced, monkeypatch):
+    """CPD_FUSE=0 at solve time runs the unfused plan on the same (fused-planned)
+    problem; both agree with the oracle's corner push (Algorithm 1 uses the same
+    primal/dual pair) and termination."""
+    lp, olp, P, *_ = forced
+    assert P.plan_info()["fused_rows"] >= 2
+    xo, yo, ro = oracle.solve(olp, oracle.default_params(max_iters=3000))
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("CPD_FUSE", fuse)
+        S = cpd.Solver(P, max_iters=3000)
+        r = S.solve()
+        assert r["status"] == ro["status"] and abs(r["iterations"] - ro["iterations"]) <= max(1, ro["iterations"] // 100)
+        assert r["pobj"] == pytest.approx(ro["pobj"], rel=1e-6)
+        S = cpd.Solver(P)
+        S.set_iterate(xo, yo)
+        rc, _, _ = S.corner_push(seed=3, max_iters=400, min_iters=10 ** 9)
+        xh, _, _, rco, _, _, _ = oracle.corner_push(olp, xo, yo, seed=3, max_iters=400, min_iters=10 ** 9)
+        xg, _ = S.get_iterate()
+        assert rc["iterations"] == rco["iterations"] == 400
+        assert close(xg, xh), (fuse, worst(xg, xh))
