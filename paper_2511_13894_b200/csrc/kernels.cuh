@@ -1050,6 +1050,9 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
     // fixed summation order: the warp's slices in order, then a fixed lane tree)
     constexpr bool FUSE = FZ && FuseRole<Epi>::v == 1 && NV == 1;
     const int hotd = FUSE ? M.hotd : 0;
+    // (measured slower on C5, profiles/r02_kernel_iterations.md: the hottest rows'
+    // accumulators in registers — spills at the 64-register cap; the last round's hot
+    // entries parked in shared memory before the epilogue — less L1 for the gathers)
     double* hacc = yhot + NV * hot + (threadIdx.x >> 5) * (hotd * 32);
     for (int h = 0; h < hotd; ++h) hacc[h * 32 + lane] = 0.0;
     __syncthreads();
