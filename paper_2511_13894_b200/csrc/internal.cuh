@@ -77,6 +77,7 @@ struct Plan {
     // hot-row fusion: rows 0..hotd-1 formed by the primal step; the fused dual step's
     // dense items without them
     int32_t hotd = 0;
+    int64_t hot_nnz = 0;                  // entries of rows 0..hotd-1 (the fused dual step skips them)
     DBuf<PlanEntry> dense_ent_f;
     DBuf<int32_t> dense_ptr_f;
     int32_t dense_maxitems_f = 0;

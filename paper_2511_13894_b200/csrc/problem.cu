@@ -313,6 +313,7 @@ void build_plan(int32_t rows, int32_t cols, const std::vector<int32_t>& rp, cons
         int32_t D = 0;
         while (D < hotd_req && D < nl && lrows[D] == D && is_heavy[D]) ++D;
         plan.hotd = D;
+        plan.hot_nnz = D > 0 ? (int64_t)rp[D] - rp[0] : 0;
         if (D > 0) {
             std::vector<PlanEntry> fent;
             std::vector<int32_t> fptr(nhb + 1, 0);

@@ -1466,9 +1466,15 @@ struct cpd_solver {
             if (base == "restart_apply") return 24 * n + 48 * m;
             return -1.0;
         }
-        if (base == "primal_step_AT") return 12 * nnz + 4 * (nr + 1) + 8 * mr + 40 * n + bnd + 12 * pz;
+        // hot-row fusion: the primal step forms the top hotd rows' products from the
+        // entries it streams anyway (+8 B per per-warp partial written, read back by
+        // the dual step) and the dual step never reads those rows' entries
+        const bool fz = fuse_ok(P);
+        const double hz = fz ? (double)P->A.plan.hot_nnz : 0.0;
+        const double hp = fz ? 8.0 * P->A.plan.hotd * cx.hot_stride : 0.0;
+        if (base == "primal_step_AT") return 12 * nnz + 4 * (nr + 1) + 8 * mr + 40 * n + bnd + 12 * pz + hp;
         if (base == "dual_step_A")
-            return 12 * (nnz - pz) + 4 * (mr + 1) + 8 * nr + 56 * m + (P->push_on ? 16.0 * mr : 0.0);
+            return 12 * (nnz - pz - hz) + 4 * (mr + 1) + 8 * nr + 56 * m + (P->push_on ? 16.0 * mr : 0.0) + hp;
         if (base == "check_eval_AT")
             return 12 * nnz + 4 * (nr + 1) + (prm.restart ? 16 : 8) * mr + 32 * n + bnd + (corner ? 16 * n : 0);
         if (base == "check_eval_A") return 12 * nnz + 4 * (mr + 1) + 8 * nr + 40 * m;
