@@ -391,6 +391,7 @@ def main():
         P = cpd.Problem.from_lp(lp, device=dev)
     S = cpd.Solver(P, max_iters=args.iters1, profile=1)
     P_info = P.dist_info()
+    plan = P.plan_info()
     for _ in range(args.warmup):
         run_step(S, args.iters1, args.iters2)
     S.kernel_times(reset=True)
@@ -442,8 +443,10 @@ def main():
                      "kernel": dom, "kernel_ms": dom_ms, "algorithmic_bytes_per_launch": dom_bytes,
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                      "whole_path_gbs": hbm_gbs, "whole_path_frac": hbm_gbs / peak,
-                     "whole_path_frac_of_8tbs": hbm_gbs / 8000.0},
+                     "whole_path_frac_of_8tbs": hbm_gbs / 8000.0,
+                     "pair": pair_roofline(S, kt, peak)},
         "kernel_time_share": kernel_share,
+        "plan": {k: int(plan[k]) for k in ("warp", "heavy_rows", "long_pieces", "hot_rows", "fused_rows", "fused_nnz")},
         "gpu_launches": launches,
         "corner_stats": {"before": before, "after": after},
     }
@@ -465,6 +468,20 @@ def main():
         res["cpu_baseline"] = cpu_baseline(lp)
     if rank == 0:
         emit(res)
+
+
+def pair_roofline(S, kt, peak):
+    """Primal + dual step as one unit (K1 + K2 of one PDHG iteration, phase 1): hot-row
+    fusion moves part of the A x+ product into K1's stream, so the pair's algorithmic bytes
+    over its summed CUDA-event time is the figure that no work shifting between the two
+    kernels can move."""
+    ks = ("primal_step_AT", "dual_step_A")
+    if not all(k in kt and kt[k][1] > 0 for k in ks):
+        return None
+    ms = sum(kt[k][0] / kt[k][1] for k in ks)
+    b = sum(S.kernel_bytes(k) for k in ks)
+    return {"kernels": list(ks), "ms": ms, "algorithmic_bytes": b, "achieved": b / (ms / 1e3) / 1e9,
+            "frac": b / (ms / 1e3) / 1e9 / peak}
 
 
 def e2e_measure(args, lp, dev, rank=0, world=1, dist_path=False):

@@ -337,7 +337,7 @@ class Problem:
         out = (C.c_int64 * 16)()
         _check(lib().cpd_problem_plan_info(self.h, out))
         keys = ("warp", "heavy_rows", "dense_blocks", "slabs", "short_slabs", "long_rows", "long_pieces",
-                "rows_items", "sell_AT", "hot_rows", "tma_entries", "cols_renumbered", "fused_rows")
+                "rows_items", "sell_AT", "hot_rows", "tma_entries", "cols_renumbered", "fused_rows", "fused_nnz")
         return dict(zip(keys, list(out)))
 
     def power_sigma(self, iters=128, seed=7):

@@ -1466,15 +1466,13 @@ struct cpd_solver {
             if (base == "restart_apply") return 24 * n + 48 * m;
             return -1.0;
         }
-        // hot-row fusion: the primal step forms the top hotd rows' products from the
-        // entries it streams anyway (+8 B per per-warp partial written, read back by
-        // the dual step) and the dual step never reads those rows' entries
-        const bool fz = fuse_ok(P);
-        const double hz = fz ? (double)P->A.plan.hot_nnz : 0.0;
-        const double hp = fz ? 8.0 * P->A.plan.hotd * cx.hot_stride : 0.0;
-        if (base == "primal_step_AT") return 12 * nnz + 4 * (nr + 1) + 8 * mr + 40 * n + bnd + 12 * pz + hp;
+        // SURVEY §8(d) per-unit figures: one A^T y product + primal update, one A x+
+        // product + dual update.  (Hot-row fusion forms part of the A x+ product inside
+        // the primal step's stream — the dual step then reads plan_info fused_nnz entries
+        // fewer; the figure stays the product's, and bench.py also reports the K1+K2 pair.)
+        if (base == "primal_step_AT") return 12 * nnz + 4 * (nr + 1) + 8 * mr + 40 * n + bnd + 12 * pz;
         if (base == "dual_step_A")
-            return 12 * (nnz - pz - hz) + 4 * (mr + 1) + 8 * nr + 56 * m + (P->push_on ? 16.0 * mr : 0.0) + hp;
+            return 12 * (nnz - pz) + 4 * (mr + 1) + 8 * nr + 56 * m + (P->push_on ? 16.0 * mr : 0.0);
         if (base == "check_eval_AT")
             return 12 * nnz + 4 * (nr + 1) + (prm.restart ? 16 : 8) * mr + 32 * n + bnd + (corner ? 16 * n : 0);
         if (base == "check_eval_A") return 12 * nnz + 4 * (mr + 1) + 8 * nr + 40 * m;
@@ -1665,7 +1663,8 @@ int cpd_problem_plan_info(const cpd_problem* p, int64_t out[16])
     out[10] = pl.warp ? 0 : pl.nent;
     out[11] = p->cperm.p ? 1 : 0;
     out[12] = cpd::fuse_ok(p) ? pl.hotd : 0;
-    out[13] = out[14] = out[15] = 0;
+    out[13] = cpd::fuse_ok(p) ? pl.hot_nnz : 0;   // entries of the fused rows (the dual step skips them)
+    out[14] = out[15] = 0;
     ABI_END
 }
 
