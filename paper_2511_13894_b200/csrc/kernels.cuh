@@ -1979,6 +1979,7 @@ template <bool PE>
 struct EpiPrimalH {
     static constexpr int NS = 3;   // ||xh - x||^2, ||xh - x_a||^2, #nonfinite(xh)
     static constexpr int NVEC = PE ? 5 : 3;
+    static constexpr int FUSE = 1;   // hot-row fusion: row() returns xh_j, the dual step's gathered value
     const double* c;
     Bounds bd;
     PingPong X;
@@ -1999,8 +2000,8 @@ struct EpiPrimalH {
     {
         return v == 0 ? c : v == 1 ? xc : v == 2 ? xa : v == 3 ? bd.l : bd.u;
     }
-    __device__ __forceinline__ void row(int j, const double* s, const double* const* vin, int li,
-                                        double* acc) const
+    __device__ __forceinline__ double row(int j, const double* s, const double* const* vin, int li,
+                                          double* acc) const
     {
         const double x = vin[1][li];
         double lo = bd.l0, hi = bd.u0;
@@ -2015,6 +2016,7 @@ struct EpiPrimalH {
         acc[0] += (h - x) * (h - x);
         acc[1] += (h - a) * (h - a);
         acc[2] += isfinite(h) ? 0.0 : 1.0;
+        return h;
     }
     __device__ void finalize(const double* tot, Ctl* ctl) const
     {
@@ -2029,6 +2031,7 @@ struct EpiPrimalH {
 struct EpiDualH {
     static constexpr int NS = 6;   // ||b - A xh||^2, b^T yh, ||yh - y||^2, <yh - y, A xh - A x>, ||yh - y_a||^2, #nonfinite
     static constexpr int NVEC = 5;
+    static constexpr int FUSE = 2;   // the fused rows' sums come from the primal step's partials
     const double* b;
     double *y, *ax, *yh, *axh;
     const double *ya, *axa;

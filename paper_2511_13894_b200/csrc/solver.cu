@@ -876,6 +876,7 @@ struct cpd_solver {
             elem(cx, std::max(n, m), orr, gr, false);
             rec(ev1, NODE_RESTART);
         }
+        cx.fuse = fuse_ok(P);   // primal step forms the hot rows' A xh products (as for R-PDHG)
         for (int s = 0; s < K; ++s) {
             const int n1 = NODE_K0 + 2 * s, n2 = n1 + 1;
             const Gate g1{GATE_K1, s, n1, active.p}, g2{GATE_K2, s, n2, active.p};
@@ -895,6 +896,7 @@ struct cpd_solver {
             pass<1>(cx, 0, fixed(XH.p), none(), e2, g2);
             rec(ev1, n2);
         }
+        cx.fuse = false;
     }
 
     // ---------------------------------------------------------- one batch

@@ -231,3 +231,43 @@ def test_hot_row_fusion_solve_time_switch(forced, monkeypatch):
         xg, _ = S.get_iterate()
         assert rc["iterations"] == rco["iterations"] == 400
         assert close(xg, xh), (fuse, worst(xg, xh))
+
+
+@pytest.mark.parametrize("hotd", ["0", "6", "16"])
+@pytest.mark.parametrize("pid", [0, 1])
+def test_hot_row_fusion_halpern_lockstep(hotd, pid, monkeypatch):
+    """Hot-row fusion under the reflected restarted Halpern method (NEXT-1): the fused
+    primal step forms A xh of the longest rows from xh_j, the dual step's k_finish sums
+    those partials — Halpern iterates (z = T-sequence, T(z) returned) within 1e-9 of the
+    oracle over 1000 iterations with restarts, PID off and on; the corner push (Algorithm
+    1 on the Halpern pair) with the fused rows against the oracle's."""
+    for k, v in FORCE.items():
+        monkeypatch.setenv(k, v)
+    monkeypatch.setenv("CPD_HOTD", hotd)
+    lp = lpgen.config("c5-s")
+    olp = oracle.OracleLP(lp)
+    P = cpd.Problem.from_lp(lp)
+    assert P.plan_info()["fused_rows"] == min(int(hotd), P.plan_info()["heavy_rows"])
+    eta = 0.9 / oracle.power_sigma(olp)
+    kw = dict(step_size=eta, restart=1, method=1, pid=pid)
+    S = cpd.Solver(P, **kw)
+    R = oracle.Run(olp, oracle.default_params(**kw), mode=oracle.MODE_NONE)
+    k = 0
+    for target in (1, 2, 64, 65, 300, 1000):
+        S.step(target - k)
+        R.run(target - k)
+        k = target
+        xg, yg = S.get_iterate()
+        xo, yo = R.get_z()
+        assert close(xg, xo) and close(yg, yo), (hotd, pid, k, worst(xg, xo), worst(yg, yo))
+    assert R.restart_state()["restarts"] >= 1
+    if pid == 1 and hotd == "6":
+        xo, yo, _ = oracle.solve(olp, oracle.default_params(max_iters=500, method=1, pid=1))
+        S = cpd.Solver(P, method=1, pid=1)
+        S.set_iterate(xo, yo)
+        rc, _, _ = S.corner_push(seed=3, max_iters=300, min_iters=10 ** 9)
+        xh, _, _, rco, _, _, _ = oracle.corner_push(olp, xo, yo, params=oracle.default_params(method=1, pid=1),
+                                                    seed=3, max_iters=300, min_iters=10 ** 9)
+        xg, _ = S.get_iterate()
+        assert rc["iterations"] == rco["iterations"] == 300
+        assert close(xg, xh), worst(xg, xh)

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--libs", default=_build.LIB)
     ap.add_argument("--iters", type=int, default=256)
     ap.add_argument("--corner", type=int, default=0)
+    ap.add_argument("--method", type=int, default=0, help="0 R-PDHG, 1 reflected restarted Halpern")
     ap.add_argument("--env", default="", help="';'-separated variants of K=V,K=V env settings per run")
     a = ap.parse_args()
     t = time.time()
@@ -34,7 +35,7 @@ def main():
         _build.LIB = path
         cpd._lib = None
         P = cpd.Problem.from_lp(lp)
-        S = cpd.Solver(P, step_size=1e-3, profile=1, max_iters=a.iters)
+        S = cpd.Solver(P, step_size=1e-3, profile=1, max_iters=a.iters, method=a.method)
         S.step(64)
         S.kernel_times(reset=True)
         t0 = time.time()
