@@ -241,6 +241,16 @@ int cpd_solver_counters(const cpd_solver *s, int64_t out[4]);
 /* Algorithmic bytes one launch of kernel `name` moves (DESIGN.md byte model). */
 int cpd_kernel_bytes(const cpd_solver *s, const char *name, double *bytes);
 
+/* Device-memory cache (not a paper operation: the library's allocator).
+ * Buffers a destroyed problem or solver freed are kept per device in exact-size bins
+ * and reused after a device synchronisation (at most CPD_MEMCACHE_MB of idle memory,
+ * default a quarter of the device; env CPD_MEMCACHE=0 bypasses it).  cached_bytes
+ * reports the idle bytes held for `device`; release frees them (cudaFree) — call it
+ * before handing the memory to another allocator in the same process.  Errors:
+ * CPD_E_ARG for a bad device ordinal or a NULL out pointer. */
+int cpd_memcache_info(int32_t device, int64_t *cached_bytes);
+int cpd_memcache_release(int32_t device);
+
 /* ------------------------------------------------------------------ inequality rows
  * Row senses ("handled implicitly"):
  * sense[m] (GLOBAL rows, int8) 0 '=' (A_i x = b_i), 1 '<=' (A_i x <= b_i), 2 '>='.

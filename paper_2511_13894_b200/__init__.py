@@ -34,6 +34,7 @@ DECLARED_SYMBOLS = [
     "cpd_partition", "cpd_nccl_get_unique_id", "cpd_problem_create_dist", "cpd_problem_dist_info",
     "cpd_problem_scale", "cpd_problem_get_scaling", "cpd_problem_set_senses", "cpd_problem_plan_info",
     "cpd_dist_layout", "cpd_dual_corner_push", "cpd_corner_decide",
+    "cpd_memcache_info", "cpd_memcache_release",
 ]
 
 
@@ -118,6 +119,8 @@ def lib():
             "cpd_compute_stats": (C.c_int, [P, P, P, P, P, D, I64, I32, C.POINTER(Stats)]),
             "cpd_get_kernel_times": (C.c_int, [P, P, P, P, I32, C.POINTER(I32), I32]),
             "cpd_kernel_bytes": (C.c_int, [P, C.c_char_p, C.POINTER(D)]),
+            "cpd_memcache_info": (C.c_int, [I32, C.POINTER(I64)]),
+            "cpd_memcache_release": (C.c_int, [I32]),
             "cpd_solver_counters": (C.c_int, [P, P]),
             "cpd_partition": (C.c_int, [I32, I32, P, P, I32, I32, P]),
             "cpd_dist_layout": (C.c_int, [I32, I32, P, P, I32, I32, I32, P]),
@@ -225,6 +228,18 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().cpd_nccl_get_unique_id(buf))
     return buf.raw
+
+
+def memcache_info(device=0) -> int:
+    """cpd_memcache_info: idle bytes the library's device-memory cache holds."""
+    b = C.c_int64()
+    _check(lib().cpd_memcache_info(int(device), C.byref(b)))
+    return b.value
+
+
+def memcache_release(device=0):
+    """cpd_memcache_release: cudaFree every idle cached buffer of `device`."""
+    _check(lib().cpd_memcache_release(int(device)))
 
 
 class Problem:

@@ -27,6 +27,13 @@ struct Error : std::runtime_error {
                                std::string(#call) + ": " + cudaGetErrorString(e_));            \
     } while (0)
 
+// Device-memory cache behind DBuf (devmem.cu): exact-size reuse after a device
+// synchronisation, so repeated problem creations do not re-map multi-GB buffers.
+cudaError_t dev_alloc(void** p, size_t bytes);
+void dev_free(void* p, size_t bytes);
+void dev_trim();
+size_t dev_cached_bytes();
+
 // Device buffer with RAII.
 template <class T>
 struct DBuf {
@@ -39,11 +46,11 @@ struct DBuf {
     {
         free();
         n = count;
-        if (count) CPD_CUDA(cudaMalloc(&p, sizeof(T) * count + 64));
+        if (count) CPD_CUDA(dev_alloc(reinterpret_cast<void**>(&p), sizeof(T) * count + 64));
     }
     void free()
     {
-        if (p) cudaFree(p);
+        if (p) dev_free(p, sizeof(T) * n + 64);
         p = nullptr;
         n = 0;
     }

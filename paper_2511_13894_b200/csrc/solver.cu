@@ -1972,6 +1972,28 @@ int cpd_solver_counters(const cpd_solver* s, int64_t out[4])
     ABI_END
 }
 
+int cpd_memcache_info(int32_t device, int64_t* cached_bytes)
+{
+    ABI_BEGIN
+    int ndev = 0;
+    CPD_CUDA(cudaGetDeviceCount(&ndev));
+    if (!cached_bytes || device < 0 || device >= ndev) return fail(CPD_E_ARG, "bad device or NULL argument");
+    CPD_CUDA(cudaSetDevice(device));
+    *cached_bytes = (int64_t)cpd::dev_cached_bytes();
+    ABI_END
+}
+
+int cpd_memcache_release(int32_t device)
+{
+    ABI_BEGIN
+    int ndev = 0;
+    CPD_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(CPD_E_ARG, "bad device ordinal");
+    CPD_CUDA(cudaSetDevice(device));
+    cpd::dev_trim();
+    ABI_END
+}
+
 int cpd_kernel_bytes(const cpd_solver* s, const char* name, double* bytes)
 {
     ABI_BEGIN
