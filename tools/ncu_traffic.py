@@ -2,7 +2,7 @@
 dram read+write bytes and duration per launch of the primal step (K1) and of the
 whole dual step (K2 = every kernel from the one after K1 through k_finish<EpiDual>:
 k_csrw segments, k_dense, k_finish), keyed by the solver's kernel names (bench.py
-`roofline.traffic`).  Usage: python tools/ncu_traffic.py REPORT CONFIG [OUT]"""
+`roofline.traffic`).  Usage: python tools/ncu_traffic.py REPORT CONFIG [OUT] [SOURCE_HASH]"""
 import csv
 import json
 import os
@@ -13,7 +13,9 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 
          "msecond": 1e-3, "ms": 1e-3, "nsecond": 1e-9}
 
 
-def main(rep, config, out="profiles/ncu_traffic.json"):
+def main(rep, config, out="profiles/ncu_traffic.json", src_hash=None):
+    """src_hash: the benchmarked sources' hash (bench.py roofline.traffic_source) when
+    the report was captured on a snapshot older than the working tree."""
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     hdr, units = rows[0], rows[1]
@@ -45,7 +47,7 @@ def main(rep, config, out="profiles/ncu_traffic.json"):
     data = json.load(open(out)) if os.path.exists(out) else {}
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from paper_2511_13894_b200 import _build
-    data[config] = {"source_hash": _build.source_hash()}
+    data[config] = {"source_hash": src_hash or _build.source_hash()}
     for k, g in groups.items():
         if not g:
             continue
