@@ -24,7 +24,7 @@ def main():
     xo = torch.empty(lp.n, dtype=torch.float64, pin_memory=True).numpy()
     yo = torch.empty(lp.m, dtype=torch.float64, pin_memory=True).numpy()
     zo = torch.empty(lp.n, dtype=torch.float64, pin_memory=True).numpy()
-    for rep in range(3):
+    for rep in range(int(os.environ.get('REPS', '3'))):
         T = [time.perf_counter()]
         P = cpd.Problem(lp.m, lp.n, AT=(pin["ATp"], pin["ATj"], pin["ATx"]), b=pin["b"], c=pin["c"], lb=pin["lb"],
                         ub=pin["ub"])
@@ -38,11 +38,12 @@ def main():
         cpd._check(cpd.lib().cpd_get_iterate(S.h, xo.ctypes.data, yo.ctypes.data, zo.ctypes.data, cpd.HOST))
         T.append(time.perf_counter())
         S.close()
+        T.append(time.perf_counter())
         P.close()
         torch.cuda.synchronize(); T.append(time.perf_counter())
-        names = ("create", "solver", "solve", "corner", "d2h", "teardown")
+        names = ("create", "solver", "solve", "corner", "d2h", "solver close", "problem close")
         print(f"rep {rep}: " + " | ".join(f"{n} {1e3 * (T[i + 1] - T[i]):.0f} ms" for i, n in enumerate(names)),
-              flush=True)
+              f" | cached {cpd.memcache_info(0) / 2**30:.1f} GiB", flush=True)
 
 
 if __name__ == "__main__":
