@@ -298,6 +298,26 @@ __device__ __forceinline__ double ld_stream(const double* p)
     return __ldcs(p);
 #endif
 }
+__device__ __forceinline__ int2 ld_stream(const int2* p)
+{
+#if CPD_NOALLOC
+    int2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+#else
+    return __ldcs(p);
+#endif
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p)
+{
+#if CPD_NOALLOC
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+#else
+    return __ldcs(p);
+#endif
+}
 
 // Bulk L2 prefetch of a byte range (cp.async.bulk.prefetch.L2, sm_90+): one
 // instruction, no registers or shared memory held, fire and forget.  The streamed
@@ -1093,8 +1113,8 @@ k_sell(DevSell M, VecSel vs0, VecSel vs1, Epi epi, Gate gate, Ctl* ctl, double* 
                 for (int u = 0; u < SELL_U; u += 2) {
                     const bool ok = k0 + u < len;   // len even: both of the pair
                     const int64_t q = sell_pos(k0 + u, lane);
-                    const int2 c2 = ok ? __ldcs(reinterpret_cast<const int2*>(cb + q)) : make_int2(-1, -1);
-                    const double2 a2 = ok ? __ldcs(reinterpret_cast<const double2*>(vb + q)) : make_double2(0.0, 0.0);
+                    const int2 c2 = ok ? ld_stream(reinterpret_cast<const int2*>(cb + q)) : make_int2(-1, -1);
+                    const double2 a2 = ok ? ld_stream(reinterpret_cast<const double2*>(vb + q)) : make_double2(0.0, 0.0);
                     cc[u] = c2.x;
                     cc[u + 1] = c2.y;
                     aa[u] = a2.x;

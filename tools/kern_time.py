@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--iters", type=int, default=256)
     ap.add_argument("--corner", type=int, default=0)
     ap.add_argument("--method", type=int, default=0, help="0 R-PDHG, 1 reflected restarted Halpern")
+    ap.add_argument("--noprof", action="store_true", help="no per-kernel events: wall it/s only")
     ap.add_argument("--env", default="", help="';'-separated variants of K=V,K=V env settings per run")
     a = ap.parse_args()
     t = time.time()
@@ -35,7 +36,7 @@ def main():
         _build.LIB = path
         cpd._lib = None
         P = cpd.Problem.from_lp(lp)
-        S = cpd.Solver(P, step_size=1e-3, profile=1, max_iters=a.iters, method=a.method)
+        S = cpd.Solver(P, step_size=1e-3, profile=0 if a.noprof else 1, max_iters=a.iters, method=a.method)
         S.step(64)
         S.kernel_times(reset=True)
         t0 = time.time()
