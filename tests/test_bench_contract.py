@@ -37,3 +37,21 @@ def test_gpus_n_self_launches_ranks():
     assert len(lines) == 1, out.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["impl"] == "reference" and d["value"] > 0
+
+
+def test_pair_roofline_arithmetic():
+    """roofline.pair = (K1 + K2 algorithmic bytes) / (summed per-launch event times) / peak,
+    None when either kernel did not run."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    class FakeSolver:
+        def kernel_bytes(self, name):
+            return {"primal_step_AT": 3.79e9, "dual_step_A": 3.28e9}[name]
+
+    kt = {"primal_step_AT": (69.0, 100), "dual_step_A": (82.7, 100)}   # (total ms, launches)
+    p = bench.pair_roofline(FakeSolver(), kt, 6550.7)
+    assert abs(p["ms"] - 1.517) < 1e-9
+    assert abs(p["achieved"] - 7.07e9 / 1.517e-3 / 1e9) < 1e-6
+    assert abs(p["frac"] - p["achieved"] / 6550.7) < 1e-12
+    assert bench.pair_roofline(FakeSolver(), {"primal_step_AT": (69.0, 100)}, 6550.7) is None
