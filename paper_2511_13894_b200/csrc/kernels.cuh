@@ -70,6 +70,10 @@ constexpr int DCHUNK = CPD_DCHUNK;   // k_dense: entries per item (balances the 
 #endif
 constexpr int TPB_D = CPD_TPB_D;
 constexpr int FIN_SPLIT = 1024;
+#ifndef CPD_FIN_G
+#define CPD_FIN_G 8
+#endif
+constexpr int FIN_G = CPD_FIN_G;   // k_finish lanes per (non-heavy) long row
 constexpr int TPB_F = 256;       // k_finish threads per CTA (1024 measured slower: 52 vs 45 us)
 constexpr int HOT_ROWS = 4096;
 #ifndef CPD_HOTY_FUSED
@@ -943,22 +947,31 @@ k_finish(DevPlan P, Epi epi, Gate gate, Ctl* ctl, double* bpart, unsigned* ctr, 
         }
     }
     {
-        const int lane = threadIdx.x & 31;
+        // the other long rows have few partials (< 131,072 nnz: at most ~70 pieces), so
+        // FIN_G lanes sum one row (lane-strided, then the xor tree inside the group: a
+        // fixed order) and a warp finishes 32 / FIN_G rows at once
+        constexpr int G = FIN_G;
+        const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
         const int nw = gridDim.x * (TPB_F / 32);
-        for (int h = P.nfin_heavy + ((blockIdx.x * TPB_F + threadIdx.x) >> 5); h < P.nlong; h += nw) {
-            const int l = P.long_ents[h];
+        for (int h0 = P.nfin_heavy + ((blockIdx.x * TPB_F + threadIdx.x) >> 5) * (32 / G); h0 < P.nlong;
+             h0 += nw * (32 / G)) {
+            const int h = h0 + sub;
+            const bool ok = h < P.nlong;
+            const int l = ok ? P.long_ents[h] : 0;
             double sm[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) sm[v] = 0.0;
-            const int64_t t0 = (int64_t)P.long_ptr[l] * P.pslot, t1 = (int64_t)P.long_ptr[l + 1] * P.pslot;
-            for (int64_t t = t0 + lane; t < t1; t += 32)
+            if (ok) {
+                const int64_t t0 = (int64_t)P.long_ptr[l] * P.pslot, t1 = (int64_t)P.long_ptr[l + 1] * P.pslot;
+                for (int64_t t = t0 + sl; t < t1; t += G)
 #pragma unroll
-                for (int v = 0; v < NV; ++v) sm[v] += __ldcg(&P.lpart[t * 2 + v]);
+                    for (int v = 0; v < NV; ++v) sm[v] += __ldcg(&P.lpart[t * 2 + v]);
+            }
 #pragma unroll
             for (int v = 0; v < NV; ++v)
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sm[v] += __shfl_xor_sync(0xffffffffu, sm[v], o);
-            if (lane == 0) {
+                for (int o = G / 2; o > 0; o >>= 1) sm[v] += __shfl_xor_sync(0xffffffffu, sm[v], o);
+            if (ok && sl == 0) {
                 const int r = P.long_row[l];
                 e.row(r, sm, vin, r, acc);
             }
